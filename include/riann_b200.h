@@ -1,0 +1,165 @@
+/*
+ * riann_b200.h -- C ABI of the B200-native RIANN per-frame ANN-field query.
+ *
+ * The reference (/root/reference/pkg/src/riann, pure Python) has no FFI for
+ * this path: its boundary is the module-level Python API.  Each entry point
+ * below names the reference function it replaces (file:line); the Python
+ * package paper_1508_07953_b200 binds these with ctypes (INTEGRATION.md shows
+ * the binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no C++ or torch types cross the ABI.
+ *  - Every int-returning call returns RIANN_OK or an error code; the message is
+ *    riann_last_error() (thread-local).  Codes map to the reference's
+ *    exception types (errors.py:4-17 plus ValueError/IndexError).
+ *  - Host pointers unless a flag says RIANN_F_DEVICE_PTRS.  Calls on one
+ *    context are serialised by the caller; one context per GPU.
+ *  - Floating point: every distance is the reference's float64 expression
+ *    (patches.py:151-159) evaluated with individually rounded IEEE ops in
+ *    numpy's pairwise-summation order, so results are bit-identical.
+ */
+#ifndef RIANN_B200_H
+#define RIANN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RIANN_ABI_VERSION 1
+
+enum {
+    RIANN_OK = 0,
+    RIANN_E_VALUE = 1,       /* ValueError        (search.py:42-48, engine.py:75-78) */
+    RIANN_E_DIMENSION = 2,   /* DimensionError    (engine.py:111-119, search.py:105-108) */
+    RIANN_E_INDEX = 3,       /* IndexError        (search.py:73-74, :110-111) */
+    RIANN_E_CAPACITY = 4,    /* ModelCapacityError (model.py:252-257): device memory */
+    RIANN_E_UNSUPPORTED = 5, /* metric_id != 0, >2^32 key words, ... (no fallback) */
+    RIANN_E_CUDA = 6,        /* CUDA runtime failure */
+    RIANN_E_STATE = 7        /* call order (no model / no tables / no field) */
+};
+
+/* flags for riann_process_frame */
+#define RIANN_F_TEMPORAL 1u     /* compute temporal_change vs the units kept from the previous frame */
+#define RIANN_F_DEVICE_PTRS 2u  /* frame / prev / outputs are device pointers on the ctx device */
+#define RIANN_F_ASYNC 4u        /* do not synchronise (device-pointer mode only); stats invalid until riann_sync */
+#define RIANN_F_KEEP_UNITS 8u   /* keep this frame's units as the next frame's prev units */
+
+typedef struct riann_ctx riann_ctx;
+
+/* FrameStats (engine.py:56-69) as integers plus the float64 temporal change;
+ * mean_candidates = sum_cand_final / queries (engine.py:183). */
+typedef struct {
+    uint64_t total_rings;
+    uint64_t total_distance_evals;
+    uint64_t sum_cand_final;
+    uint64_t sum_first_ring;   /* sum |S_1|: roofline byte count */
+    uint64_t queries;
+    double temporal_change;
+} riann_frame_stats;
+
+int riann_abi_version(void);
+const char *riann_last_error(void);
+
+/* ---- context ---------------------------------------------------------- */
+int riann_ctx_create(int device, riann_ctx **out);
+int riann_ctx_destroy(riann_ctx *ctx);
+/* the context's CUDA stream (cudaStream_t), for event timing by the caller */
+void *riann_ctx_stream(riann_ctx *ctx);
+int riann_sync(riann_ctx *ctx);
+/* device bytes currently held by the context */
+uint64_t riann_ctx_device_bytes(riann_ctx *ctx);
+
+/* ---- model (model.py:56-83 ReferenceModel) ----------------------------- */
+/* refs: (n, dim) float32 unit rows; patch (pw, ph); channels; metric_id must
+ * be 0 (Euclidean, patches.py:164-179).  dim must equal pw*ph*channels. */
+int riann_model_set_refs(riann_ctx *ctx, const float *refs, int64_t n, int dim,
+                         int pw, int ph, int channels, int metric_id);
+/* Upload reference-built sorted tables (compute_sorted_lists output):
+ * sorted_dist float32 (n, n) (the reference's float64 values are exactly
+ * float32), sorted_idx int32 (n, n).  Replaces model.py:162-189's result. */
+int riann_model_set_tables(riann_ctx *ctx, const float *sorted_dist,
+                           const int32_t *sorted_idx);
+/* K3: build the sorted tables on the GPU, bit-identical to
+ * compute_sorted_lists (model.py:162-189). */
+int riann_model_build_tables(riann_ctx *ctx);
+/* Download rows [row0, row0+rows) of the sorted tables. */
+int riann_model_get_tables(riann_ctx *ctx, int64_t row0, int64_t rows,
+                           float *sorted_dist, int32_t *sorted_idx);
+
+/* ---- frame path (engine.py:93-187 process_frame) ----------------------- */
+/* frame: (H, W, C) float32 rows [gy0, gy0 + gh + ph - 1) of the full frame,
+ * i.e. a row band with a (ph-1)-row halo; the band's grid rows are
+ * [gy0, gy0 + H - ph + 1) of a grid gw = W - pw + 1 wide.  RNG keys use the
+ * global (x, y) = (g % gw, gy0 + g / gw) and t (engine.py:124, 136-142).
+ * prev_idx: (gh_band, gw) previous indices, or NULL to use the field kept on
+ * the device by the previous call.  out_idx / out_dist may be NULL (the field
+ * stays device-resident).  seed < 2^64. */
+int riann_process_frame(riann_ctx *ctx, const float *frame, int H, int W, int C,
+                        int gy0, const int32_t *prev_idx, uint64_t seed,
+                        uint32_t t, int L, double alpha, int max_rings,
+                        unsigned flags, int32_t *out_idx, double *out_dist,
+                        riann_frame_stats *stats);
+/* Upload prev units (rows, dim) for the next RIANN_F_TEMPORAL frame
+ * (process_frame's prev_unit argument, engine.py:163-171). */
+int riann_set_prev_units(riann_ctx *ctx, const float *units, int64_t rows, int dim);
+/* Read back the device-resident field of the last frame. */
+int riann_field_get(riann_ctx *ctx, int32_t *idx, double *dist, int64_t count);
+
+/* extract_patches + normalize_rows (patches.py:65-115) on the GPU:
+ * unit (Q, dim) float32, norms (Q,) float64 (either may be NULL). */
+int riann_frame_units(riann_ctx *ctx, const float *frame, int H, int W, int C,
+                      float *unit, double *norms);
+/* normalize_rows (patches.py:100-115) on arbitrary rows. */
+int riann_normalize_rows(riann_ctx *ctx, const float *values, int64_t m, int dim,
+                         float *unit, double *norms);
+/* float64-input variant (the reference converts any input to float64). */
+int riann_normalize_rows_f64(riann_ctx *ctx, const double *values, int64_t m,
+                             int dim, float *unit, double *norms);
+/* EuclideanMetric.one_to_many (patches.py:151-159): q (dim,), rows (k, dim). */
+int riann_one_to_many(riann_ctx *ctx, const float *q, const float *rows,
+                      int64_t k, int dim, double *out);
+int riann_one_to_many_f64(riann_ctx *ctx, const double *q, const double *rows,
+                          int64_t k, int dim, double *out);
+/* extract_patches (patches.py:65-97): raw windows at `stride`, row-major
+ * dy*pw+dx, plane-major channels; out (gh*gw, pw*ph*C). */
+int riann_extract_patches(riann_ctx *ctx, const float *frame, int H, int W,
+                          int C, int pw, int ph, int stride, float *out);
+
+/* ---- single / batched queries (search.py:63-151) ----------------------- */
+/* ring_candidates (search.py:63-80) on the model's table: window [lo, hi) of
+ * row `anchor` and (if out != NULL, capacity n) its index slice. */
+int riann_ring_candidates(riann_ctx *ctx, int64_t anchor, double d, double eps,
+                          int64_t *lo, int64_t *hi, int32_t *out);
+/* riann_query (search.py:83-151) for m queries with explicit RNG keys:
+ * key words of query i are key_words[key_off[i] .. key_off[i+1]) (numpy
+ * SeedSequence entropy words, <= 16 per key).  Optional outputs may be NULL.
+ * scanned: capacity m * (n + 1); query i writes S u {prev} ascending at
+ * scanned + i*(n+1), its length in scanned_len[i]. */
+int riann_query_batch(riann_ctx *ctx, const float *queries, const int32_t *prev,
+                      const uint32_t *key_words, const int64_t *key_off, int64_t m,
+                      int L, double alpha, int max_rings, int32_t *out_idx,
+                      double *out_dist, int32_t *out_rings, int64_t *out_evals,
+                      int64_t *out_cand, int64_t *out_first, int32_t *scanned,
+                      int64_t *scanned_len);
+
+/* ---- exact comparator (evaluation.py:24-50) ----------------------------- */
+int riann_exact_nn_batch(riann_ctx *ctx, const float *queries, int64_t m,
+                         int32_t *out_idx, double *out_dist);
+int riann_exact_field(riann_ctx *ctx, const float *frame, int H, int W, int C,
+                      int32_t *out_idx, double *out_dist);
+
+/* ---- host helpers ------------------------------------------------------ */
+/* init_field indices (engine.py:72-82): numpy default_rng(seed).integers(0,
+ * n, (gh, gw), int32), bit-identical; seed given as SeedSequence words. */
+int riann_init_field(int gw, int gh, int64_t n, const uint32_t *seed_words,
+                     int nwords, int32_t *out);
+/* numpy pairwise float64 sum (for the host side of multi-band reductions) */
+double riann_pairwise_sum(const double *a, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,987 @@
+// riann_b200.cu -- C ABI (include/riann_b200.h) over the sm_100a kernels.
+//
+// Host side of the drop-in boundary: owns device memory for one GPU, keeps the
+// reference model and the per-position field resident across frames, and
+// launches K1 (units) -> K2 (query) -> pairwise reduction per frame on the
+// context's stream.  No CPU fallback: every compute entry point runs on the
+// GPU or returns an error.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_segmented_radix_sort.cuh>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "riann_b200.h"
+#include "riann_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            if (e_ == cudaErrorMemoryAllocation) {                                             \
+                cudaGetLastError();                                                            \
+                return fail(RIANN_E_CAPACITY, "%s: %s", #call, cudaGetErrorString(e_));        \
+            }                                                                                  \
+            return fail(RIANN_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                             \
+        }                                                                                      \
+    } while (0)
+
+#define RET(x)                 \
+    do {                       \
+        int r_ = (x);          \
+        if (r_) return r_;     \
+    } while (0)
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes)
+    {
+        if (bytes <= cap) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t b = bytes < 256 ? 256 : bytes;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return fail(RIANN_E_CAPACITY, "cudaMalloc(%zu bytes): %s", b, cudaGetErrorString(e));
+        }
+        cap = b;
+        return 0;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T *as() const
+    {
+        return static_cast<T *>(p);
+    }
+};
+
+// numpy pairwise tree over Q values (host-built once per Q).
+struct PwTree {
+    int64_t q = -1;
+    int nleaves = 0, nlevels = 0, nnodes = 0;
+    DevBuf leaf_start, leaf_len, leaf_node, level_off, inner, left, right, node_val;
+
+    int build(int64_t Q)
+    {
+        if (Q == q) return 0;
+        std::vector<int64_t> ls;
+        std::vector<int32_t> ll, ln, L, R, depth;
+        std::vector<std::vector<int32_t>> levels;
+        // iterative DFS: node ids assigned in creation order, root 0
+        struct Item {
+            int64_t s, n;
+            int id, dep;
+        };
+        std::vector<Item> st;
+        L.push_back(-1);
+        R.push_back(-1);
+        st.push_back({0, Q, 0, 0});
+        int nid = 1;
+        while (!st.empty()) {
+            Item it = st.back();
+            st.pop_back();
+            if (it.n <= 128) {
+                ls.push_back(it.s);
+                ll.push_back((int32_t)it.n);
+                ln.push_back(it.id);
+            } else {
+                int64_t h = it.n / 2;
+                h -= h % 8;
+                int a = nid++, b = nid++;
+                L.push_back(-1);
+                R.push_back(-1);
+                L.push_back(-1);
+                R.push_back(-1);
+                L[it.id] = a;
+                R[it.id] = b;
+                if ((int)levels.size() <= it.dep) levels.resize(it.dep + 1);
+                levels[it.dep].push_back(it.id);
+                st.push_back({it.s, h, a, it.dep + 1});
+                st.push_back({it.s + h, it.n - h, b, it.dep + 1});
+            }
+        }
+        std::vector<int32_t> off(1, 0), inner_ids;
+        for (int d = (int)levels.size() - 1; d >= 0; d--) {
+            for (int x : levels[d]) inner_ids.push_back(x);
+            off.push_back((int32_t)inner_ids.size());
+        }
+        nleaves = (int)ls.size();
+        nlevels = (int)levels.size();
+        nnodes = nid;
+        RET(leaf_start.ensure(ls.size() * 8));
+        RET(leaf_len.ensure(ll.size() * 4));
+        RET(leaf_node.ensure(ln.size() * 4));
+        RET(level_off.ensure(off.size() * 4));
+        RET(inner.ensure((inner_ids.size() + 1) * 4));
+        RET(left.ensure(L.size() * 4));
+        RET(right.ensure(R.size() * 4));
+        RET(node_val.ensure((size_t)nid * 8));
+        CK(cudaMemcpy(leaf_start.p, ls.data(), ls.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(leaf_len.p, ll.data(), ll.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(leaf_node.p, ln.data(), ln.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(level_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+        if (!inner_ids.empty())
+            CK(cudaMemcpy(inner.p, inner_ids.data(), inner_ids.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(left.p, L.data(), L.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(right.p, R.data(), R.size() * 4, cudaMemcpyHostToDevice));
+        q = Q;
+        return 0;
+    }
+};
+
+}  // namespace
+
+struct riann_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sms = 0;
+    int smem_optin = 0;
+    // model
+    int64_t n = 0;
+    int dim = 0, pw = 0, ph = 0, C = 1;
+    bool tables = false;
+    DevBuf refs, sdist, sidx;
+    // frame path
+    DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
+    DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
+    int cur_units = 0;
+    bool have_prev_units = false;
+    int64_t prev_units_rows = 0;
+    int cur_fld = 0;
+    int64_t field_count = -1;
+    PwTree tree;
+
+    int use()
+    {
+        CK(cudaSetDevice(device));
+        return 0;
+    }
+    uint64_t bytes() const
+    {
+        uint64_t b = refs.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
+                     fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap;
+        return b;
+    }
+};
+
+namespace {
+
+int bitmap_words(int64_t n)
+{
+    int64_t w = (n + 31) / 32;
+    w = (w + 31) / 32 * 32;
+    return (int)(w < 32 ? 32 : w);
+}
+
+template <int D>
+int launch_query_t(riann_ctx *c, rb::QueryParams &P)
+{
+    const size_t per_warp = (size_t)(P.nw + rb::HIT_CAP) * 4;
+    int wpb = 8;
+    while (wpb > 1 && per_warp * wpb > (size_t)c->smem_optin) wpb--;
+    if (per_warp * wpb > (size_t)c->smem_optin)
+        return fail(RIANN_E_CAPACITY, "model n=%lld needs %zu B shared memory per warp", (long long)c->n, per_warp);
+    const size_t smem = per_warp * wpb;
+    CK(cudaFuncSetAttribute(rb::query_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, rb::query_kernel<D>, wpb * 32, smem));
+    if (bps < 1) bps = 1;
+    int64_t blocks = (int64_t)c->sms * bps;
+    int64_t need = (P.Q + wpb - 1) / wpb;
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    RET(c->overflow.ensure((size_t)blocks * wpb * (size_t)c->n * 4));
+    P.overflow = c->overflow.as<int32_t>();
+    rb::query_kernel<D><<<(unsigned)blocks, wpb * 32, smem, c->stream>>>(P);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int launch_query(riann_ctx *c, rb::QueryParams &P)
+{
+    P.nw = bitmap_words(c->n);
+    switch (c->dim) {
+    case 16: return launch_query_t<16>(c, P);
+    case 64: return launch_query_t<64>(c, P);
+    case 192: return launch_query_t<192>(c, P);
+    default: return launch_query_t<0>(c, P);
+    }
+}
+
+int check_model(riann_ctx *c, bool need_tables)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (c->n <= 0) return fail(RIANN_E_STATE, "no reference model uploaded");
+    if (need_tables && !c->tables) return fail(RIANN_E_STATE, "model has no sorted tables");
+    return 0;
+}
+
+int check_err(riann_ctx *c)
+{
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h == rb::ERR_PREV_RANGE) return fail(RIANN_E_INDEX, "prev_index out of range for %lld references", (long long)c->n);
+    if (h == rb::ERR_USED_OVERFLOW)
+        return fail(RIANN_E_UNSUPPORTED, "more than 32 used anchors remained in the candidate set");
+    if (h) return fail(RIANN_E_CUDA, "kernel error %d", h);
+    return 0;
+}
+
+int launch_units(riann_ctx *c, const float *frame, int H, int W, int C, float *unit, double *norms,
+                 const float *prev_unit, double *tc)
+{
+    rb::UnitsParams U;
+    U.frame = frame;
+    U.H = H;
+    U.W = W;
+    U.C = C;
+    U.pw = c->pw;
+    U.ph = c->ph;
+    U.gw = W - c->pw + 1;
+    U.Q = (int64_t)U.gw * (H - c->ph + 1);
+    U.dim = c->dim;
+    U.unit = unit;
+    U.norms = norms;
+    U.prev_unit = prev_unit;
+    U.tc = tc;
+    if (U.Q <= 0) return 0;
+    unsigned blocks = (unsigned)((U.Q + 127) / 128);
+    if (c->pw == 8 && c->ph == 8) rb::units_kernel<8, 8><<<blocks, 128, 0, c->stream>>>(U);
+    else rb::units_kernel<0, 0><<<blocks, 128, 0, c->stream>>>(U);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int check_frame(riann_ctx *c, int H, int W, int C)
+{
+    if (C != c->C)
+        return fail(RIANN_E_DIMENSION, "frame has %d channels, model expects %d", C, c->C);
+    if (W < c->pw || H < c->ph)
+        return fail(RIANN_E_DIMENSION, "frame %dx%d smaller than patch %dx%d", W, H, c->pw, c->ph);
+    return 0;
+}
+
+// ---- host numpy RNG (init_field) ----
+typedef unsigned __int128 u128;
+const u128 HPCG_MULT = ((u128)2549297995355413924ULL << 64) | (u128)4865540595714422341ULL;
+struct HostPcg {
+    u128 s, inc;
+    int has;
+    uint32_t buf;
+};
+uint32_t h_hash(uint32_t v, uint32_t &hc)
+{
+    v ^= hc;
+    hc *= 0x931e8875u;
+    v *= hc;
+    v ^= v >> 16;
+    return v;
+}
+uint32_t h_mix(uint32_t x, uint32_t y)
+{
+    uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+    return r ^ (r >> 16);
+}
+void h_seed(HostPcg &g, const uint32_t *w, int nw)
+{
+    uint32_t pool[4], hc = 0x43b0d7e5u;
+    for (int i = 0; i < 4; i++) pool[i] = h_hash(i < nw ? w[i] : 0u, hc);
+    for (int s = 0; s < 4; s++)
+        for (int d = 0; d < 4; d++)
+            if (s != d) pool[d] = h_mix(pool[d], h_hash(pool[s], hc));
+    for (int s = 4; s < nw; s++)
+        for (int d = 0; d < 4; d++) pool[d] = h_mix(pool[d], h_hash(w[s], hc));
+    uint32_t st[8], hb = 0x8b51f9ddu;
+    for (int i = 0; i < 8; i++) {
+        uint32_t v = pool[i & 3];
+        v ^= hb;
+        hb *= 0x58f38dedu;
+        v *= hb;
+        v ^= v >> 16;
+        st[i] = v;
+    }
+    uint64_t w0 = st[0] | ((uint64_t)st[1] << 32), w1 = st[2] | ((uint64_t)st[3] << 32);
+    uint64_t w2 = st[4] | ((uint64_t)st[5] << 32), w3 = st[6] | ((uint64_t)st[7] << 32);
+    g.inc = ((((u128)w2 << 64) | w3) << 1) | 1u;
+    g.s = g.inc;
+    g.s += ((u128)w0 << 64) | w1;
+    g.s = g.s * HPCG_MULT + g.inc;
+    g.has = 0;
+    g.buf = 0;
+}
+uint32_t h_next32(HostPcg &g)
+{
+    if (g.has) {
+        g.has = 0;
+        return g.buf;
+    }
+    g.s = g.s * HPCG_MULT + g.inc;
+    uint64_t x = (uint64_t)(g.s >> 64) ^ (uint64_t)g.s;
+    unsigned rot = (unsigned)(g.s >> 122);
+    uint64_t v = (x >> rot) | (x << ((64u - rot) & 63u));
+    g.has = 1;
+    g.buf = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+uint64_t h_integers(HostPcg &g, uint64_t k)
+{
+    uint64_t rng = k - 1;
+    if (rng == 0) return 0;
+    if (rng == 0xFFFFFFFFull) return h_next32(g);
+    uint32_t excl = (uint32_t)rng + 1u;
+    uint64_t m = (uint64_t)h_next32(g) * excl;
+    uint32_t left = (uint32_t)m;
+    if (left < excl) {
+        uint32_t thr = (0xFFFFFFFFu - (uint32_t)rng) % excl;
+        while (left < thr) {
+            m = (uint64_t)h_next32(g) * excl;
+            left = (uint32_t)m;
+        }
+    }
+    return m >> 32;
+}
+
+double h_pairwise(const double *a, int64_t n)
+{
+    if (n < 8) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; i++) s += a[i];
+        return s;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) s += a[i];
+        return s;
+    }
+    int64_t h = n / 2;
+    h -= h % 8;
+    return h_pairwise(a, h) + h_pairwise(a + h, n - h);
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int riann_abi_version(void) { return RIANN_ABI_VERSION; }
+const char *riann_last_error(void) { return g_err.c_str(); }
+
+int riann_ctx_create(int device, riann_ctx **out)
+{
+    if (!out) return fail(RIANN_E_VALUE, "out is null");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(RIANN_E_VALUE, "device %d out of range (%d devices)", device, ndev);
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(RIANN_E_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+    riann_ctx *c = new riann_ctx();
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(RIANN_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
+    if (c->err.ensure(64) || c->stats.ensure(64) || c->tc_sum.ensure(64) || c->small.ensure(64)) {
+        delete c;
+        return RIANN_E_CAPACITY;
+    }
+    *out = c;
+    return 0;
+}
+
+int riann_ctx_destroy(riann_ctx *c)
+{
+    if (!c) return 0;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    DevBuf *bufs[] = {&c->refs, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
+                      &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
+                      &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
+                      &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,
+                      &c->tree.leaf_start, &c->tree.leaf_len, &c->tree.leaf_node, &c->tree.level_off,
+                      &c->tree.inner, &c->tree.left, &c->tree.right, &c->tree.node_val};
+    for (DevBuf *b : bufs) b->release();
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return 0;
+}
+
+void *riann_ctx_stream(riann_ctx *c) { return c ? (void *)c->stream : nullptr; }
+
+int riann_sync(riann_ctx *c)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    RET(c->use());
+    CK(cudaStreamSynchronize(c->stream));
+    return check_err(c);
+}
+
+uint64_t riann_ctx_device_bytes(riann_ctx *c) { return c ? c->bytes() : 0; }
+
+int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, int pw, int ph, int channels,
+                         int metric_id)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (metric_id != 0)
+        return fail(RIANN_E_UNSUPPORTED, "metric id %d: only the Euclidean metric (id 0) has a GPU path", metric_id);
+    if (n < 1) return fail(RIANN_E_VALUE, "need at least one reference, got n=%lld", (long long)n);
+    if (n > 0x7fffffffLL) return fail(RIANN_E_CAPACITY, "n=%lld exceeds int32 indices", (long long)n);
+    if (dim < 1 || pw < 1 || ph < 1 || channels < 1 || (int64_t)pw * ph * channels != dim)
+        return fail(RIANN_E_DIMENSION, "dim %d != patch %dx%d x %d channels", dim, pw, ph, channels);
+    RET(c->use());
+    CK(cudaStreamSynchronize(c->stream));
+    c->sdist.release();
+    c->sidx.release();
+    c->tables = false;
+    RET(c->refs.ensure((size_t)n * dim * 4));
+    CK(cudaMemcpyAsync(c->refs.p, refs, (size_t)n * dim * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->n = n;
+    c->dim = dim;
+    c->pw = pw;
+    c->ph = ph;
+    c->C = channels;
+    c->field_count = -1;
+    c->have_prev_units = false;
+    return 0;
+}
+
+int riann_model_set_tables(riann_ctx *c, const float *sd, const int32_t *si)
+{
+    RET(check_model(c, false));
+    RET(c->use());
+    const size_t bytes = (size_t)c->n * c->n * 4;
+    RET(c->sdist.ensure(bytes));
+    RET(c->sidx.ensure(bytes));
+    CK(cudaMemcpyAsync(c->sdist.p, sd, bytes, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->sidx.p, si, bytes, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->tables = true;
+    return 0;
+}
+
+int riann_model_build_tables(riann_ctx *c)
+{
+    RET(check_model(c, false));
+    RET(c->use());
+    const int64_t n = c->n;
+    const size_t tbytes = (size_t)n * n * 4;
+    RET(c->sdist.ensure(tbytes));
+    RET(c->sidx.ensure(tbytes));
+    // row batches bounded by ~1 GiB of unsorted keys+values
+    int64_t rb_rows = (int64_t)((1ull << 30) / ((size_t)n * 8));
+    if (rb_rows < 1) rb_rows = 1;
+    if (rb_rows > n) rb_rows = n;
+    if ((int64_t)rb_rows * n > 0x7fffffffLL) rb_rows = 0x7fffffffLL / n;
+    RET(c->keys.ensure((size_t)rb_rows * n * 8));
+    uint32_t *keys_in = c->keys.as<uint32_t>();
+    int32_t *vals_in = reinterpret_cast<int32_t *>(keys_in + (size_t)rb_rows * n);
+    // segment offsets r*n
+    std::vector<int> offs(rb_rows + 1);
+    for (int64_t r = 0; r <= rb_rows; r++) offs[r] = (int)(r * n);
+    DevBuf d_off;
+    RET(d_off.ensure(offs.size() * 4));
+    CK(cudaMemcpy(d_off.p, offs.data(), offs.size() * 4, cudaMemcpyHostToDevice));
+    size_t temp_bytes = 0;
+    CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, temp_bytes, keys_in, (uint32_t *)nullptr, vals_in,
+                                                 (int32_t *)nullptr, (int)(rb_rows * n), (int)rb_rows,
+                                                 d_off.as<int>(), d_off.as<int>() + 1, 0, 32, c->stream));
+    DevBuf temp;
+    RET(temp.ensure(temp_bytes));
+    for (int64_t r0 = 0; r0 < n; r0 += rb_rows) {
+        const int64_t rows = (r0 + rb_rows <= n) ? rb_rows : n - r0;
+        const unsigned blocks = (unsigned)((rows + 7) / 8 < (int64_t)c->sms * 8 ? (rows + 7) / 8 : (int64_t)c->sms * 8);
+        switch (c->dim) {
+        case 16: rb::table_keys_kernel<16><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
+        case 64: rb::table_keys_kernel<64><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
+        case 192: rb::table_keys_kernel<192><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
+        default: rb::table_keys_kernel<0><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
+        }
+        CK(cudaGetLastError());
+        uint32_t *kout = reinterpret_cast<uint32_t *>(c->sdist.as<float>() + (size_t)r0 * n);
+        int32_t *vout = c->sidx.as<int32_t>() + (size_t)r0 * n;
+        CK(cub::DeviceSegmentedRadixSort::SortPairs(temp.p, temp_bytes, keys_in, kout, vals_in, vout,
+                                                     (int)(rows * n), (int)rows, d_off.as<int>(),
+                                                     d_off.as<int>() + 1, 0, 32, c->stream));
+        rb::self_first_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, c->stream>>>(kout, vout, n, r0, rows);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    temp.release();
+    d_off.release();
+    c->keys.release();
+    c->tables = true;
+    return 0;
+}
+
+int riann_model_get_tables(riann_ctx *c, int64_t row0, int64_t rows, float *sd, int32_t *si)
+{
+    RET(check_model(c, true));
+    if (row0 < 0 || rows < 0 || row0 + rows > c->n) return fail(RIANN_E_INDEX, "rows out of range");
+    RET(c->use());
+    const size_t off = (size_t)row0 * c->n, cnt = (size_t)rows * c->n;
+    if (sd) CK(cudaMemcpyAsync(sd, c->sdist.as<float>() + off, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (si) CK(cudaMemcpyAsync(si, c->sidx.as<int32_t>() + off, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int riann_set_prev_units(riann_ctx *c, const float *units, int64_t rows, int dim)
+{
+    RET(check_model(c, false));
+    if (dim != c->dim) return fail(RIANN_E_DIMENSION, "prev_unit dim %d != model dim %d", dim, c->dim);
+    RET(c->use());
+    const int slot = c->cur_units ^ 1;
+    RET(c->units[slot].ensure((size_t)rows * dim * 4));
+    CK(cudaMemcpyAsync(c->units[slot].p, units, (size_t)rows * dim * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->have_prev_units = true;
+    c->prev_units_rows = rows;
+    return 0;
+}
+
+int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, int gy0, const int32_t *prev_idx,
+                        uint64_t seed, uint32_t t, int L, double alpha, int max_rings, unsigned flags,
+                        int32_t *out_idx, double *out_dist, riann_frame_stats *stats)
+{
+    RET(check_model(c, true));
+    RET(check_frame(c, H, W, C));
+    if (L < 1) return fail(RIANN_E_VALUE, "L must be >= 1, got %d", L);
+    if (!(alpha > 0.0 && alpha < 1.0)) return fail(RIANN_E_VALUE, "alpha must lie in (0, 1), got %g", alpha);
+    if (max_rings < 1) return fail(RIANN_E_VALUE, "max_rings must be >= 1, got %d", max_rings);
+    if (gy0 < 0) return fail(RIANN_E_VALUE, "negative band offset");
+    RET(c->use());
+    const bool dev = (flags & RIANN_F_DEVICE_PTRS) != 0;
+    const int gw = W - c->pw + 1, gh = H - c->ph + 1;
+    const int64_t Q = (int64_t)gw * gh;
+    const size_t fbytes = (size_t)H * W * C * 4;
+    const float *d_frame = frame;
+    if (!dev) {
+        RET(c->frame.ensure(fbytes));
+        CK(cudaMemcpyAsync(c->frame.p, frame, fbytes, cudaMemcpyHostToDevice, c->stream));
+        d_frame = c->frame.as<float>();
+    }
+    // previous field
+    const int32_t *d_prev = nullptr;
+    const int in_slot = c->cur_fld, out_slot = c->cur_fld ^ 1;
+    if (prev_idx) {
+        if (dev) {
+            d_prev = prev_idx;
+        } else {
+            RET(c->fld_idx[in_slot].ensure((size_t)Q * 4));
+            CK(cudaMemcpyAsync(c->fld_idx[in_slot].p, prev_idx, (size_t)Q * 4, cudaMemcpyHostToDevice, c->stream));
+            d_prev = c->fld_idx[in_slot].as<int32_t>();
+        }
+    } else {
+        if (c->field_count != Q)
+            return fail(RIANN_E_STATE, "no device-resident field of %lld positions (have %lld)", (long long)Q,
+                        (long long)c->field_count);
+        d_prev = c->fld_idx[in_slot].as<int32_t>();
+    }
+    int32_t *d_idx = nullptr;
+    double *d_dist = nullptr;
+    if (dev && out_idx && out_dist) {
+        d_idx = out_idx;
+        d_dist = out_dist;
+    } else {
+        RET(c->fld_idx[out_slot].ensure((size_t)Q * 4));
+        RET(c->fld_dist.ensure((size_t)Q * 8));
+        d_idx = c->fld_idx[out_slot].as<int32_t>();
+        d_dist = c->fld_dist.as<double>();
+    }
+    // K1: units (+ temporal change per position)
+    const bool temporal = (flags & RIANN_F_TEMPORAL) != 0;
+    if (temporal && (!c->have_prev_units || c->prev_units_rows != Q))
+        return fail(RIANN_E_DIMENSION, "prev_unit rows %lld do not match %lld positions",
+                    (long long)(c->have_prev_units ? c->prev_units_rows : 0), (long long)Q);
+    const int us = c->cur_units;
+    RET(c->units[us].ensure((size_t)Q * c->dim * 4));
+    if (temporal) RET(c->tc.ensure((size_t)Q * 8));
+    RET(launch_units(c, d_frame, H, W, C, c->units[us].as<float>(), nullptr,
+                     temporal ? c->units[us ^ 1].as<float>() : nullptr, temporal ? c->tc.as<double>() : nullptr));
+    // K2: queries
+    CK(cudaMemsetAsync(c->stats.p, 0, 32, c->stream));
+    CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
+    rb::QueryParams P;
+    memset(&P, 0, sizeof P);
+    P.refs = c->refs.as<float>();
+    P.sdist = c->sdist.as<float>();
+    P.sidx = c->sidx.as<int32_t>();
+    P.n = c->n;
+    P.dim = c->dim;
+    P.units = c->units[us].as<float>();
+    P.prev = d_prev;
+    P.Q = Q;
+    P.seed_lo = (uint32_t)seed;
+    P.seed_hi = (uint32_t)(seed >> 32);
+    P.seed_nw = (seed >> 32) ? 2 : 1;
+    P.gw = gw;
+    P.gy0 = gy0;
+    P.t = t;
+    P.L = L;
+    P.alpha = alpha;
+    P.max_rings = max_rings;
+    P.out_idx = d_idx;
+    P.out_dist = d_dist;
+    P.stats = c->stats.as<unsigned long long>();
+    P.err = c->err.as<int>();
+    if (Q > 0) RET(launch_query(c, P));
+    if (temporal && Q > 0) {
+        RET(c->tree.build(Q));
+        rb::PwTreeParams T;
+        T.vals = c->tc.as<double>();
+        T.nleaves = c->tree.nleaves;
+        T.leaf_start = c->tree.leaf_start.as<int64_t>();
+        T.leaf_len = c->tree.leaf_len.as<int32_t>();
+        T.leaf_node = c->tree.leaf_node.as<int32_t>();
+        T.nlevels = c->tree.nlevels;
+        T.level_off = c->tree.level_off.as<int32_t>();
+        T.inner_node = c->tree.inner.as<int32_t>();
+        T.left = c->tree.left.as<int32_t>();
+        T.right = c->tree.right.as<int32_t>();
+        T.node_val = c->tree.node_val.as<double>();
+        T.out = c->tc_sum.as<double>();
+        rb::pw_tree_kernel<<<1, 1024, 0, c->stream>>>(T);
+        CK(cudaGetLastError());
+    }
+    if (!dev) {
+        if (out_idx) CK(cudaMemcpyAsync(out_idx, d_idx, (size_t)Q * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (out_dist) CK(cudaMemcpyAsync(out_dist, d_dist, (size_t)Q * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (!(dev && d_idx == out_idx)) {
+        c->cur_fld = out_slot;
+        c->field_count = Q;
+    } else {
+        c->field_count = -1;
+    }
+    if (flags & RIANN_F_KEEP_UNITS) {
+        c->cur_units ^= 1;
+        c->have_prev_units = true;
+        c->prev_units_rows = Q;
+    }
+    if ((flags & RIANN_F_ASYNC) && dev) return 0;
+    unsigned long long hs[4] = {0, 0, 0, 0};
+    double tcv = 0.0;
+    CK(cudaMemcpyAsync(hs, c->stats.p, 32, cudaMemcpyDeviceToHost, c->stream));
+    if (temporal && Q > 0) CK(cudaMemcpyAsync(&tcv, c->tc_sum.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    RET(check_err(c));
+    if (stats) {
+        stats->total_rings = hs[0];
+        stats->total_distance_evals = hs[1];
+        stats->sum_cand_final = hs[2];
+        stats->sum_first_ring = hs[3];
+        stats->queries = (uint64_t)Q;
+        stats->temporal_change = tcv;
+    }
+    return 0;
+}
+
+int riann_field_get(riann_ctx *c, int32_t *idx, double *dist, int64_t count)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (c->field_count != count) return fail(RIANN_E_STATE, "no device field of %lld positions", (long long)count);
+    RET(c->use());
+    if (idx) CK(cudaMemcpyAsync(idx, c->fld_idx[c->cur_fld].p, (size_t)count * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (dist) CK(cudaMemcpyAsync(dist, c->fld_dist.p, (size_t)count * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int riann_frame_units(riann_ctx *c, const float *frame, int H, int W, int C, float *unit, double *norms)
+{
+    RET(check_model(c, false));
+    RET(check_frame(c, H, W, C));
+    RET(c->use());
+    const int64_t Q = (int64_t)(W - c->pw + 1) * (H - c->ph + 1);
+    const size_t fbytes = (size_t)H * W * C * 4;
+    RET(c->frame.ensure(fbytes));
+    CK(cudaMemcpyAsync(c->frame.p, frame, fbytes, cudaMemcpyHostToDevice, c->stream));
+    DevBuf u, nr;
+    RET(u.ensure((size_t)Q * c->dim * 4));
+    RET(nr.ensure((size_t)Q * 8));
+    RET(launch_units(c, c->frame.as<float>(), H, W, C, u.as<float>(), nr.as<double>(), nullptr, nullptr));
+    if (unit) CK(cudaMemcpyAsync(unit, u.p, (size_t)Q * c->dim * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (norms) CK(cudaMemcpyAsync(norms, nr.p, (size_t)Q * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    u.release();
+    nr.release();
+    return 0;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <class T>
+int normalize_rows_t(riann_ctx *c, const T *values, int64_t m, int dim, float *unit, double *norms)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (dim < 1 || m < 0) return fail(RIANN_E_DIMENSION, "bad shape (%lld, %d)", (long long)m, dim);
+    if (m == 0) return 0;
+    RET(c->use());
+    DevBuf v, u, nr;
+    RET(v.ensure((size_t)m * dim * sizeof(T)));
+    RET(u.ensure((size_t)m * dim * 4));
+    RET(nr.ensure((size_t)m * 8));
+    CK(cudaMemcpyAsync(v.p, values, (size_t)m * dim * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    rb::normalize_rows_kernel<T><<<(unsigned)((m + 127) / 128), 128, 0, c->stream>>>(v.as<T>(), m, dim, u.as<float>(),
+                                                                                     nr.as<double>());
+    CK(cudaGetLastError());
+    if (unit) CK(cudaMemcpyAsync(unit, u.p, (size_t)m * dim * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (norms) CK(cudaMemcpyAsync(norms, nr.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+template <class T>
+int one_to_many_t(riann_ctx *c, const T *q, const T *rows, int64_t k, int dim, double *out)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (dim < 1 || k < 0) return fail(RIANN_E_DIMENSION, "bad shape (%lld, %d)", (long long)k, dim);
+    if (k == 0) return 0;
+    RET(c->use());
+    DevBuf dq, dr, dout;
+    RET(dq.ensure((size_t)dim * sizeof(T)));
+    RET(dr.ensure((size_t)k * dim * sizeof(T)));
+    RET(dout.ensure((size_t)k * 8));
+    CK(cudaMemcpyAsync(dq.p, q, (size_t)dim * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dr.p, rows, (size_t)k * dim * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    rb::one_to_many_kernel<T><<<(unsigned)((k + 127) / 128), 128, 0, c->stream>>>(dq.as<T>(), dr.as<T>(), k, dim,
+                                                                                  dout.as<double>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout.p, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int riann_normalize_rows(riann_ctx *c, const float *values, int64_t m, int dim, float *unit, double *norms)
+{
+    return normalize_rows_t<float>(c, values, m, dim, unit, norms);
+}
+
+int riann_normalize_rows_f64(riann_ctx *c, const double *values, int64_t m, int dim, float *unit, double *norms)
+{
+    return normalize_rows_t<double>(c, values, m, dim, unit, norms);
+}
+
+int riann_one_to_many(riann_ctx *c, const float *q, const float *rows, int64_t k, int dim, double *out)
+{
+    return one_to_many_t<float>(c, q, rows, k, dim, out);
+}
+
+int riann_one_to_many_f64(riann_ctx *c, const double *q, const double *rows, int64_t k, int dim, double *out)
+{
+    return one_to_many_t<double>(c, q, rows, k, dim, out);
+}
+
+int riann_extract_patches(riann_ctx *c, const float *frame, int H, int W, int C, int pw, int ph, int stride,
+                          float *out)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (pw < 1 || ph < 1) return fail(RIANN_E_DIMENSION, "patch size must be positive, got (%d, %d)", pw, ph);
+    if (stride < 1) return fail(RIANN_E_DIMENSION, "stride must be >= 1, got %d", stride);
+    if (W < pw || H < ph) return fail(RIANN_E_DIMENSION, "frame %dx%d smaller than patch %dx%d", W, H, pw, ph);
+    RET(c->use());
+    const int gw = (W - pw) / stride + 1, gh = (H - ph) / stride + 1;
+    const int64_t Q = (int64_t)gw * gh;
+    const size_t fbytes = (size_t)H * W * C * 4, obytes = (size_t)Q * pw * ph * C * 4;
+    DevBuf f, o;
+    RET(f.ensure(fbytes));
+    RET(o.ensure(obytes));
+    CK(cudaMemcpyAsync(f.p, frame, fbytes, cudaMemcpyHostToDevice, c->stream));
+    rb::extract_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, c->stream>>>(f.as<float>(), W, C, pw, ph, stride, gw, Q,
+                                                                           o.as<float>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, o.p, obytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int riann_ring_candidates(riann_ctx *c, int64_t anchor, double d, double eps, int64_t *lo, int64_t *hi, int32_t *out)
+{
+    RET(check_model(c, true));
+    if (anchor < 0 || anchor >= c->n)
+        return fail(RIANN_E_INDEX, "anchor %lld out of range for %lld references", (long long)anchor, (long long)c->n);
+    if (d < 0 || eps < 0) return fail(RIANN_E_VALUE, "ring radius and width must be nonnegative");
+    RET(c->use());
+    rb::ring_window_kernel<<<1, 32, 0, c->stream>>>(c->sdist.as<float>() + (size_t)anchor * c->n, c->n, d - eps,
+                                                   d + eps, c->small.as<int64_t>());
+    CK(cudaGetLastError());
+    int64_t h[2];
+    CK(cudaMemcpyAsync(h, c->small.p, 16, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *lo = h[0];
+    *hi = h[1];
+    if (out && h[1] > h[0])
+        CK(cudaMemcpy(out, c->sidx.as<int32_t>() + (size_t)anchor * c->n + h[0], (size_t)(h[1] - h[0]) * 4,
+                      cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int riann_query_batch(riann_ctx *c, const float *queries, const int32_t *prev, const uint32_t *key_words,
+                      const int64_t *key_off, int64_t m, int L, double alpha, int max_rings, int32_t *out_idx,
+                      double *out_dist, int32_t *out_rings, int64_t *out_evals, int64_t *out_cand,
+                      int64_t *out_first, int32_t *scanned, int64_t *scanned_len)
+{
+    RET(check_model(c, true));
+    if (L < 1) return fail(RIANN_E_VALUE, "L must be >= 1, got %d", L);
+    if (!(alpha > 0.0 && alpha < 1.0)) return fail(RIANN_E_VALUE, "alpha must lie in (0, 1), got %g", alpha);
+    if (max_rings < 1) return fail(RIANN_E_VALUE, "max_rings must be >= 1, got %d", max_rings);
+    if (m <= 0) return 0;
+    for (int64_t i = 0; i < m; i++) {
+        if (prev[i] < 0 || prev[i] >= c->n)
+            return fail(RIANN_E_INDEX, "prev_index %d out of range for %lld references", prev[i], (long long)c->n);
+        if (key_off[i + 1] - key_off[i] > 16 || key_off[i + 1] < key_off[i])
+            return fail(RIANN_E_UNSUPPORTED, "rng key of %lld words (max 16)", (long long)(key_off[i + 1] - key_off[i]));
+    }
+    RET(c->use());
+    const int64_t nk = key_off[m];
+    DevBuf dq, dp, di, dd;
+    RET(dq.ensure((size_t)m * c->dim * 4));
+    RET(dp.ensure((size_t)m * 4));
+    RET(di.ensure((size_t)m * 4));
+    RET(dd.ensure((size_t)m * 8));
+    RET(c->kw.ensure((size_t)(nk + 1) * 4));
+    RET(c->koff.ensure((size_t)(m + 1) * 8));
+    CK(cudaMemcpyAsync(dq.p, queries, (size_t)m * c->dim * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dp.p, prev, (size_t)m * 4, cudaMemcpyHostToDevice, c->stream));
+    if (nk) CK(cudaMemcpyAsync(c->kw.p, key_words, (size_t)nk * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->koff.p, key_off, (size_t)(m + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+    RET(c->q_rings.ensure((size_t)m * 4));
+    RET(c->q_evals.ensure((size_t)m * 8));
+    RET(c->q_cand.ensure((size_t)m * 8));
+    RET(c->q_first.ensure((size_t)m * 8));
+    RET(c->q_scanned_len.ensure((size_t)m * 8));
+    if (scanned) RET(c->q_scanned.ensure((size_t)m * (c->n + 1) * 4));
+    CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
+    rb::QueryParams P;
+    memset(&P, 0, sizeof P);
+    P.refs = c->refs.as<float>();
+    P.sdist = c->sdist.as<float>();
+    P.sidx = c->sidx.as<int32_t>();
+    P.n = c->n;
+    P.dim = c->dim;
+    P.units = dq.as<float>();
+    P.prev = dp.as<int32_t>();
+    P.Q = m;
+    P.key_words = c->kw.as<uint32_t>();
+    P.key_off = c->koff.as<int64_t>();
+    P.gw = 1;
+    P.L = L;
+    P.alpha = alpha;
+    P.max_rings = max_rings;
+    P.out_idx = di.as<int32_t>();
+    P.out_dist = dd.as<double>();
+    P.out_rings = c->q_rings.as<int32_t>();
+    P.out_evals = c->q_evals.as<int64_t>();
+    P.out_cand = c->q_cand.as<int64_t>();
+    P.out_first = c->q_first.as<int64_t>();
+    P.scanned = scanned ? c->q_scanned.as<int32_t>() : nullptr;
+    P.scanned_len = c->q_scanned_len.as<int64_t>();
+    P.stats = nullptr;
+    P.err = c->err.as<int>();
+    RET(launch_query(c, P));
+    if (out_idx) CK(cudaMemcpyAsync(out_idx, di.p, (size_t)m * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (out_dist) CK(cudaMemcpyAsync(out_dist, dd.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (out_rings) CK(cudaMemcpyAsync(out_rings, c->q_rings.p, (size_t)m * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (out_evals) CK(cudaMemcpyAsync(out_evals, c->q_evals.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (out_cand) CK(cudaMemcpyAsync(out_cand, c->q_cand.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (out_first) CK(cudaMemcpyAsync(out_first, c->q_first.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (scanned_len) CK(cudaMemcpyAsync(scanned_len, c->q_scanned_len.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (scanned) CK(cudaMemcpyAsync(scanned, c->q_scanned.p, (size_t)m * (c->n + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+    RET(check_err(c));
+    return 0;
+}
+
+int riann_exact_nn_batch(riann_ctx *c, const float *queries, int64_t m, int32_t *out_idx, double *out_dist)
+{
+    RET(check_model(c, false));
+    if (m <= 0) return 0;
+    RET(c->use());
+    DevBuf dq, di, dd;
+    RET(dq.ensure((size_t)m * c->dim * 4));
+    RET(di.ensure((size_t)m * 4));
+    RET(dd.ensure((size_t)m * 8));
+    CK(cudaMemcpyAsync(dq.p, queries, (size_t)m * c->dim * 4, cudaMemcpyHostToDevice, c->stream));
+    unsigned blocks = (unsigned)((m + 7) / 8 < (int64_t)c->sms * 8 ? (m + 7) / 8 : (int64_t)c->sms * 8);
+    switch (c->dim) {
+    case 16: rb::exact_nn_kernel<16><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
+    case 64: rb::exact_nn_kernel<64><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
+    case 192: rb::exact_nn_kernel<192><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
+    default: rb::exact_nn_kernel<0><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_idx, di.p, (size_t)m * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(out_dist, dd.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int riann_exact_field(riann_ctx *c, const float *frame, int H, int W, int C, int32_t *out_idx, double *out_dist)
+{
+    RET(check_model(c, false));
+    RET(check_frame(c, H, W, C));
+    const int64_t Q = (int64_t)(W - c->pw + 1) * (H - c->ph + 1);
+    std::vector<float> unit((size_t)Q * c->dim);
+    RET(riann_frame_units(c, frame, H, W, C, unit.data(), nullptr));
+    return riann_exact_nn_batch(c, unit.data(), Q, out_idx, out_dist);
+}
+
+int riann_init_field(int gw, int gh, int64_t n, const uint32_t *seed_words, int nwords, int32_t *out)
+{
+    if (n < 1) return fail(RIANN_E_VALUE, "need at least one reference, got n=%lld", (long long)n);
+    if (gw < 1 || gh < 1) return fail(RIANN_E_VALUE, "empty grid %dx%d", gw, gh);
+    if (n > 0x7fffffffLL) return fail(RIANN_E_VALUE, "n too large for int32 indices");
+    HostPcg g;
+    h_seed(g, seed_words, nwords);
+    const int64_t total = (int64_t)gw * gh;
+    for (int64_t i = 0; i < total; i++) out[i] = (int32_t)h_integers(g, (uint64_t)n);
+    return 0;
+}
+
+double riann_pairwise_sum(const double *a, int64_t n) { return h_pairwise(a, n); }
+
+}  // extern "C"

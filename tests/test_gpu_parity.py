@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path through the C ABI vs the live-reference goldens
+and the CPU oracle.  Bar: bit-exact indices, float64 distances and integer
+FrameStats (the design target; BASELINE's tolerance is >= 99.9% / 1e-4 rel).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, ragged
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R():
+    import paper_1508_07953_b200 as R
+
+    return R
+
+
+def _bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+# ---------------------------------------------------------------------------
+def test_one_to_many_and_normalize_golden(R):
+    g = load_golden("golden_arith.npz")
+    for i, d in enumerate(g["dims"]):
+        d = int(d)
+        q = ragged(g["q"], g["q_off"], i)
+        r = ragged(g["r"], g["r_off"], i).reshape(-1, d)
+        got = R.EUCLIDEAN.one_to_many(q, r)
+        assert np.array_equal(_bits(got), _bits(ragged(g["d"], g["d_off"], i))), d
+        v = ragged(g["norm_in"], g["norm_in_off"], i).reshape(-1, d)
+        u, nr = R.normalize_rows(v)
+        assert np.array_equal(_bits(u), _bits(ragged(g["norm_unit"], g["norm_in_off"], i).reshape(-1, d))), d
+        assert np.array_equal(nr, ragged(g["norm_norms"], g["norm_off"], i)), d
+
+
+def test_one_to_many_float64_inputs(R, oracle_mod):
+    rng = np.random.default_rng(3)
+    q = rng.uniform(-1, 1, size=16)
+    refs = rng.uniform(-1, 1, size=(50, 16))
+    want = np.sqrt(np.sum((refs - q) ** 2, axis=1))
+    assert np.array_equal(R.EUCLIDEAN.one_to_many(q, refs), want)
+
+
+def test_sorted_tables_golden(R):
+    g = load_golden("golden_tables.npz")
+    for i, (n, d) in enumerate(g["shapes"]):
+        refs = ragged(g["refs"], g["refs_off"], i).reshape(int(n), int(d))
+        sd, si = R.compute_sorted_lists(refs)
+        assert sd.dtype == np.float64 and si.dtype == np.int32
+        assert np.array_equal(sd.ravel(), ragged(g["sdist"], g["tab_off"], i).astype(np.float64))
+        assert np.array_equal(si.ravel(), ragged(g["sidx"], g["tab_off"], i))
+
+
+def _golden_models(R, g):
+    models = []
+    for i, (n, d) in enumerate(g["model_shapes"]):
+        refs = ragged(g["models"], g["model_off"], i).reshape(int(n), int(d))
+        models.append(R.ReferenceModel.from_refs(refs, (int(d), 1)))
+    return models
+
+
+def test_riann_query_golden(R):
+    g = load_golden("golden_queries.npz")
+    models = _golden_models(R, g)
+    for c in range(len(g["mid"])):
+        m = models[int(g["mid"][c])]
+        key = tuple(int(v) for v in ragged(g["key"], g["key_off"], c))
+        p = R.SearchParams(L=int(g["L"][c]), alpha=float(g["alpha"][c]), max_rings=int(g["mr"][c]))
+        r = R.riann_query(m, ragged(g["q"], g["q_off"], c), int(g["prev"][c]), p, rng_state=key)
+        assert r.match_index == g["idx"][c], c
+        assert r.match_distance == g["dist"][c], c
+        assert r.rings_drawn == g["rings"][c], c
+        assert r.distance_evals == g["evals"][c], c
+        assert r.candidates_final == g["cand"][c], c
+        assert np.array_equal(r.scanned, ragged(g["scanned"], g["scanned_off"], c)), c
+
+
+def test_riann_query_batch_matches_single(R):
+    g = load_golden("golden_queries.npz")
+    models = _golden_models(R, g)
+    sel = [c for c in range(len(g["mid"])) if int(g["mid"][c]) == 9]
+    m = models[9]
+    qs = np.stack([ragged(g["q"], g["q_off"], c) for c in sel])
+    keys = [tuple(int(v) for v in ragged(g["key"], g["key_off"], c)) for c in sel]
+    same = [c for c in sel if g["L"][c] == 20 and g["mr"][c] == 8 and g["alpha"][c] == 0.25]
+    idx = [sel.index(c) for c in same]
+    r = R.riann_query_batch(m, qs[idx], g["prev"][same], R.SearchParams(), keys=[keys[i] for i in idx])
+    assert np.array_equal(r["idx"], g["idx"][same])
+    assert np.array_equal(_bits(r["dist"]), _bits(g["dist"][same]))
+    assert np.array_equal(r["evals"], g["evals"][same])
+
+
+# ---------------------------------------------------------------------------
+# ports of the reference's known-answer tests (test_search.py:31-114)
+@pytest.fixture()
+def tri(R):
+    s = np.float32(np.sqrt(2.0) / 2.0)
+    return R.ReferenceModel.from_refs(np.array([[1, 0], [0, 1], [s, s]], np.float32), (2, 1))
+
+
+def test_ring_windows_known_answers(R, tri):
+    assert R.ring_candidates(tri, 0, 0.765367, 0.191342).tolist() == [2]
+    assert R.ring_candidates(tri, 1, 0.0, 0.0).tolist() == [1]
+    top = float(tri.sorted_dist[0, -1])
+    assert sorted(R.ring_candidates(tri, 0, top, top).tolist()) == [0, 1, 2]
+    d = float(tri.sorted_dist[0, 1])
+    assert R.ring_candidates(tri, 0, d, 0.0).tolist() == [2]
+    with pytest.raises(IndexError):
+        R.ring_candidates(tri, 3, 0.5, 0.1)
+    with pytest.raises(ValueError):
+        R.ring_candidates(tri, 0, -0.1, 0.1)
+
+
+def test_ring_windows_brute_force(R):
+    rng = np.random.default_rng(12345)
+    rows = rng.normal(size=(80, 12))
+    rows = (rows / np.linalg.norm(rows, axis=1, keepdims=True)).astype(np.float32)
+    m = R.ReferenceModel.from_refs(rows, (12, 1))
+    for _ in range(200):
+        a = int(rng.integers(80))
+        d = float(rng.uniform(0, 1.6))
+        eps = float(rng.uniform(0, 0.4))
+        row = m.metric.one_to_many(rows[a], rows).astype(np.float32).astype(np.float64)
+        want = set(np.flatnonzero((row >= d - eps) & (row <= d + eps)).tolist())
+        assert set(R.ring_candidates(m, a, d, eps).tolist()) == want
+
+
+def test_query_known_answers(R, tri):
+    r = R.riann_query(tri, tri.refs[1], 1)
+    assert (r.match_index, r.match_distance, r.rings_drawn) == (1, 0.0, 1)
+    r = R.riann_query(tri, tri.refs[2], 0)
+    assert (r.match_index, r.match_distance, r.rings_drawn, r.candidates_final) == (2, 0.0, 1, 1)
+    assert r.scanned.tolist() == [0, 2]
+    r = R.riann_query(tri, np.zeros(2, np.float32), 0)
+    assert r.match_distance == pytest.approx(1.0, abs=1e-6)
+    tie = R.ReferenceModel.from_refs(np.array([[1, 0], [0, 1], [1, 0]], np.float32), (2, 1))
+    r = R.riann_query(tie, tie.refs[0], 2)
+    assert (r.match_index, r.match_distance) == (0, 0.0)
+    with pytest.raises(IndexError):
+        R.riann_query(tri, tri.refs[0], 3)
+    with pytest.raises(R.DimensionError):
+        R.riann_query(tri, np.ones(3, np.float32), 0)
+
+
+def test_query_accounting_and_scope(R, oracle_mod):
+    rng = np.random.default_rng(7)
+    rows = rng.normal(size=(150, 16))
+    rows = (rows / np.linalg.norm(rows, axis=1, keepdims=True)).astype(np.float32)
+    m = R.ReferenceModel.from_refs(rows, (16, 1))
+    qs, _ = R.normalize_rows(rows[rng.integers(0, 150, 300)] + rng.normal(scale=0.08, size=(300, 16)).astype(np.float32))
+    prev = rng.integers(0, 150, 300)
+    keys = [(7, k) for k in range(300)]
+    r = R.riann_query_batch(m, qs, prev, R.SearchParams(), keys=keys, scanned=True)
+    for k in range(300):
+        sc = r["scanned"][k]
+        assert r["evals"][k] == 1 + (r["rings"][k] - 1) + sc.size
+        rescan = m.metric.one_to_many(qs[k], rows[sc])
+        assert r["dist"][k] == rescan.min()
+        assert r["idx"][k] == sc[int(np.argmin(rescan))]
+        assert 1 <= r["rings"][k] <= 8
+
+
+# ---------------------------------------------------------------------------
+def test_cfg0_stream_golden(R):
+    """Config 0 end to end: every position of all 8 frames, FrameStats exact."""
+    from paper_1508_07953_b200 import workloads as W
+
+    g = load_golden("golden_cfg0.npz")
+    model = R.ReferenceModel.from_refs(g["refs"], (8, 8))
+    out = list(R.stream_fields(model, list(g["frames"]), R.SearchParams()))
+    assert len(out) == 8
+    for t, (_, fld, st) in enumerate(out):
+        assert fld.frame_t == t + 1
+        assert np.array_equal(fld.indices, g["idx"][t]), t
+        assert np.array_equal(_bits(fld.distances), _bits(g["dist"][t])), t
+        assert [st.total_rings, st.total_distance_evals, st.queries] == list(g["stats_int"][t]), t
+        assert st.mean_candidates == g["stats_f"][t][0], t
+        assert st.temporal_change == g["stats_f"][t][1], t
+    assert W.digest(model.sorted_dist.astype(np.float32), model.sorted_idx) == str(g["table_digest"])
+
+
+def test_cfg0_process_frame_host_prev_matches_stream(R):
+    g = load_golden("golden_cfg0.npz")
+    model = R.ReferenceModel.from_refs(g["refs"], (8, 8))
+    f0 = R.init_field(57, 57, model.n, seed=0)
+    a, sa = R.process_frame(g["frames"][0], f0, model, threads=1)
+    b, sb = R.process_frame(g["frames"][0], f0, model, threads=4)
+    assert np.array_equal(a.indices, g["idx"][0]) and np.array_equal(b.indices, a.indices)
+    assert np.array_equal(a.distances, b.distances) and sa == sb
+    u0 = R.frame_units(g["frames"][0], model)
+    c, sc = R.process_frame(g["frames"][1], a, model, prev_unit=u0)
+    assert np.array_equal(c.indices, g["idx"][1])
+    assert sc.temporal_change == g["stats_f"][1][1]
+
+
+def test_cfg0_exact_field_golden(R):
+    g = load_golden("golden_cfg0.npz")
+    model = R.ReferenceModel.from_refs(g["refs"], (8, 8))
+    fld = R.field_exact_oracle(g["frames"][-1], model)
+    s = int(g["exact_stride"])
+    assert np.array_equal(fld.indices.ravel()[::s], g["exact_idx"])
+    assert np.array_equal(_bits(fld.distances.ravel()[::s]), _bits(g["exact_dist"]))
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2])
+def test_vga_full_frames_match_golden_positions(R, cfg_id):
+    """Configs 1-2: all 299,409 positions per frame on the GPU; the golden
+    positions (live reference, engine.py:137-143) must match bit for bit."""
+    from paper_1508_07953_b200 import workloads as W
+
+    g = load_golden(f"golden_cfg{cfg_id}.npz")
+    cfg = W.CONFIGS[cfg_id]
+    frames = W.clip(cfg)
+    assert W.digest(frames) == str(g["frames_digest"])
+    refs = W.reference_set(cfg)
+    model = R.ReferenceModel.from_refs(refs, cfg.patch)
+    rows = g["table_rows"]
+    sd, si = model.table_rows(0, model.n)
+    assert np.array_equal(sd[rows], g["table_rows_dist"])
+    assert np.array_equal(si[rows], g["table_rows_idx"])
+    assert W.digest(sd, si) == str(g["table_digest"])
+    pos = g["positions"]
+    for t, (_, fld, st) in enumerate(R.stream_fields(model, frames, R.SearchParams())):
+        assert np.array_equal(fld.indices.ravel()[pos], g["idx"][t]), t
+        assert np.array_equal(_bits(fld.distances.ravel()[pos]), _bits(g["dist"][t])), t
+
+
+def test_rgb_small_clip_vs_oracle(R, oracle_mod):
+    """D=192 (plane-major RGB) path on a small config-3-like clip, all positions."""
+    from dataclasses import replace
+
+    from paper_1508_07953_b200 import workloads as W
+
+    cfg = replace(W.CONFIGS[3], height=48, width=72, frames=4, n_refs=2048)
+    frames = W.clip(cfg)
+    refs = W.reference_set(cfg)
+    model = R.ReferenceModel.from_refs(refs, cfg.patch, channels=3)
+    om = oracle_mod.OracleModel.build(refs)
+    sd, si = model.table_rows(0, model.n)
+    assert np.array_equal(sd, om.sorted_dist) and np.array_equal(si, om.sorted_idx)
+    gw, gh = cfg.grid
+    prev = oracle_mod.init_field_indices(gw, gh, model.n, 0)
+    prev_unit = None
+    for t, (_, fld, st) in enumerate(R.stream_fields(model, frames, R.SearchParams())):
+        idx, dist, ost, unit = oracle_mod.process_frame(om, frames[t], prev, cfg.patch, t + 1, prev_unit=prev_unit)
+        assert np.array_equal(fld.indices, idx), t
+        assert np.array_equal(_bits(fld.distances), _bits(dist)), t
+        assert st.total_rings == ost["total_rings"] and st.total_distance_evals == ost["total_distance_evals"]
+        assert st.mean_candidates == ost["mean_candidates"]
+        assert st.temporal_change == ost["temporal_change"]
+        assert st.first_ring_total == ost["sum_first_ring"]
+        prev, prev_unit = idx, unit
+
+
+def test_engine_properties(R):
+    """test_engine.py:79-169 ports: never worse, monotone on a static frame,
+    frame counter, stats counting, error paths."""
+    from paper_1508_07953_b200 import workloads as W
+
+    rng = np.random.default_rng(2)
+    frame = W.clip(W.CONFIGS[0], 1)[0][:32, :32].copy()
+    refs, _ = R.normalize_rows(R.extract_patches(frame, (4, 4)).values[rng.choice(29 * 29, 40, replace=False)])
+    model = R.ReferenceModel.from_refs(refs, (4, 4))
+    gw, gh = R.grid_shape(frame.shape, model.patch_size)
+    f0 = R.init_field(gw, gh, model.n, seed=0)
+    f1, st = R.process_frame(frame, f0, model)
+    unit = R.frame_units(frame, model)
+    dprev = np.array([model.metric(unit[g], model.refs[int(p)]) for g, p in enumerate(f0.indices.ravel())])
+    assert np.all(f1.distances.ravel() <= dprev + 1e-12)
+    assert st.queries == gw * gh and st.total_distance_evals >= 2 * st.queries
+    assert st.total_rings >= st.queries and st.temporal_change == 0.0
+    fld, prevd = R.init_field(gw, gh, model.n, seed=1), np.full((gh, gw), np.inf)
+    for k in range(5):
+        fld, _ = R.process_frame(frame, fld, model)
+        assert fld.frame_t == k + 1
+        assert np.all(fld.distances <= prevd)
+        prevd = fld.distances
+    with pytest.raises(R.DimensionError):
+        R.process_frame(frame, R.init_field(5, 5, model.n), model)
+    with pytest.raises(R.DimensionError):
+        R.process_frame(frame, f0, model, prev_unit=np.zeros((3, 16), np.float32))
+    with pytest.raises(ValueError):
+        R.process_frame(frame, f0, model, threads=0)
+    moved = np.roll(frame, 2, axis=1)
+    _, s2 = R.process_frame(moved, f1, model, prev_unit=unit)
+    u2 = R.frame_units(moved, model)
+    diff = u2.astype(np.float64) - unit.astype(np.float64)
+    assert s2.temporal_change == float(np.sum(np.sqrt(np.sum(diff * diff, axis=1))))

@@ -69,7 +69,8 @@ SIGNATURES = {
 }
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.Lock()       # guards library loading
+_ctx_lock = threading.Lock()   # guards the per-device context table
 
 
 def lib():
@@ -190,7 +191,7 @@ def context(device: int | None = None) -> Context:
     d = current_device() if device is None else int(device)
     ctx = _contexts.get(d)
     if ctx is None:
-        with _lock:
+        with _ctx_lock:
             ctx = _contexts.get(d)
             if ctx is None:
                 ctx = Context(d)

@@ -1,0 +1,393 @@
+"""Benchmark of the RIANN per-frame ANN-field query on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
+
+A step is one frame of BASELINE.json's headline workload (config 3: 1080p RGB,
+8x8x3 = 192-D patches, n = 65,536 references; 2,052,649 queries per frame).
+The frame's grid rows are split into bands, one per rank (ranks launched by
+torchrun, one process per GPU, NCCL).  Prints one JSON line on rank 0.
+
+  value   query patches/s, inputs resident in HBM (frames pre-uploaded; the
+          field and previous units device-resident), device-timed with CUDA
+          events on the library's stream, max over ranks.
+  e2e     the same metric through the public API (BandStream / stream_fields)
+          with host frames from pinned memory and the field read back to the
+          host each frame (wall clock, max over ranks; N>1 adds the NCCL field
+          gather to rank 0).
+  roofline  algorithmic bytes of the query kernel (SURVEY.md §8d formula,
+          frame read excluded) / its CUDA-event time vs MEASURED_PEAKS HBM.
+  cpu_baseline  the CPU oracle (C port of the reference, all host threads) on
+          a bounded sample of positions of the same frames.
+--impl reference times that CPU port alone (rank 0; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_1508_07953_b200 import workloads as W  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--cpu-positions", type=int, default=512)
+    ap.add_argument("--ref-positions", type=int, default=192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thr.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4)
+                          if r[5 + k].lower() in ("active", "1")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_bytes(st, dim, n):
+    """SURVEY.md §8d per-frame bytes of the query kernel (frame read excluded):
+    16 B/position (prev idx in, idx + f64 dist out) + 4 B per first-ring entry
+    + 8*ceil(log2 n) B per ring (two binary searches) + 4*D B per distance."""
+    return (16 * st.queries + 4 * st.first_ring_total + 8 * math.ceil(math.log2(n)) * st.total_rings
+            + 4 * dim * st.total_distance_evals)
+
+
+def sample_positions(gw, y0, y1, count, seed=1234):
+    """Stratified seeded sample of grid positions inside rows [y0, y1)."""
+    rng = np.random.default_rng(seed)
+    rows = np.linspace(y0, y1 - 1, num=min(count, y1 - y0), dtype=np.int64)
+    per = int(math.ceil(count / len(rows)))
+    pos = []
+    for y in rows:
+        pos.extend(int(y) * gw + rng.choice(gw, size=per, replace=False))
+    return np.array(sorted(set(pos))[:count], dtype=np.int64)
+
+
+def sample_units(frame, cfg, pos, gw):
+    from oracle import oracle as O
+
+    raw = W.patch_rows(frame, cfg.patch, pos // gw, pos % gw)
+    return O.normalize_rows(raw)[0]
+
+
+# ---------------------------------------------------------------------------
+def run_reference(a):
+    """--impl reference: the CPU port of the reference (oracle/, C, all host
+    threads) on a bounded sample of positions, steps = frames."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    cfg = W.CONFIGS[a.config]
+    gw, gh = cfg.grid
+    K, Wm = a.steps, a.warmup
+    frames = list(W.iter_clip(cfg, Wm + K))
+    refs = W.reference_set(cfg)
+    om = O.LazyOracleModel(refs) if cfg.n_refs > 8192 else O.OracleModel.build(refs)
+    pos = sample_positions(gw, 0, gh, a.ref_positions)
+    prev = O.init_field_indices(gw, gh, len(refs), 0).ravel()[pos]
+    threads = os.cpu_count() or 1
+    units = [sample_units(f, cfg, pos, gw) for f in frames]
+    # pass 1 (untimed): the trajectory; builds every table row it touches
+    # (the reference keeps its full table in RAM; rows here are its preprocessing)
+    prevs = [prev]
+    for t in range(Wm + K):
+        r = O.query_positions(om, units[t], prevs[-1], pos, gw, 0, t + 1, nthreads=threads)
+        prevs.append(r["idx"])
+    # pass 2: time each step (frame) on the warm model
+    times = []
+    for t in range(Wm + K):
+        t0 = time.perf_counter()
+        r = O.query_positions(om, units[t], prevs[t], pos, gw, 0, t + 1, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+        assert np.array_equal(r["idx"], prevs[t + 1])
+    timed = times[Wm:]
+    qps = len(pos) * K / sum(timed)
+    line = {
+        "metric": "query patches/sec per ANNF (1080p RGB, 8x8x3 patches, n=65536)",
+        "value": qps, "unit": "query patches/s", "impl": "reference",
+        "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": 1e3 * sum(timed) / K,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded blurred-noise clip, BASELINE config shape)",
+        "config": {"workload": cfg.name, "queries_per_frame": cfg.queries,
+                   "sample_positions_per_step": int(len(pos))},
+        "cpu_baseline": {"value": qps, "unit": "query patches/s", "cores": threads, "kind": "port",
+                         "sample": f"{len(pos)} stratified positions x {K} frames (after {Wm} warm-up "
+                                   f"frames) of {cfg.name}; C port of search.py:83-151 in oracle/"},
+        "e2e": {"value": qps, "unit": "query patches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import paper_1508_07953_b200 as R
+    from paper_1508_07953_b200 import _native as N
+    from paper_1508_07953_b200.bands import BandStream, band_rows, frame_band
+
+    R.set_device(local)
+    cfg = W.CONFIGS[a.config]
+    K, Wm = a.steps, a.warmup
+    gw, gh = cfg.grid
+    y0, y1 = band_rows(gh, world, rank)
+    pw, ph = cfg.patch
+    q_band = (y1 - y0) * gw
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    # ---- inputs: W warm-up + K e2e + K device-resident frames (band rows, pinned)
+    t0 = time.time()
+    total = Wm + 2 * K
+    host = []
+    for f in W.iter_clip(cfg, total):
+        band = frame_band(f, y0, y1, ph)
+        pinned = torch.empty(band.shape, dtype=torch.float32, pin_memory=True)
+        pinned.numpy()[...] = band
+        host.append(pinned)
+    refs = W.reference_set(cfg)
+    t_data = time.time() - t0
+    model = R.ReferenceModel.from_refs(refs, cfg.patch, channels=cfg.channels)
+    ctx = N.context(local)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    with ctx.lock:
+        R.model.resident(ctx, model)  # K3 table build on the GPU
+    t_tables = time.time() - t0
+    dev_frames = [host[Wm + K + k].cuda(non_blocking=True) for k in range(K)]
+    torch.cuda.synchronize()
+
+    stream = BandStream(model, gw, gh, y0, y1, R.SearchParams(), device=local)
+    # warm-up frames (frame 1 starts from the random field: the heavy frame)
+    fields = []
+    for k in range(Wm):
+        fields.append(stream.step(host[k].numpy()))
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    # ---- e2e: public API, host frames in, host field out (+ NCCL gather at N>1)
+    gathered = None
+    if world > 1:
+        gathered = torch.empty((world, (gh // world + 1) * gw * 3), dtype=torch.int32, device="cuda")
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(K):
+        idx, dst, st = stream.step(host[Wm + k].numpy())
+        fields.append((idx, dst, st))
+        if world > 1:
+            buf = torch.zeros((gh // world + 1) * gw * 3, dtype=torch.int32, device="cuda")
+            payload = np.concatenate([idx.ravel(), dst.ravel().view(np.int32)])
+            buf[: payload.size] = torch.from_numpy(payload).cuda()
+            dist.all_gather_into_tensor(gathered, buf)
+            if rank == 0:
+                gathered.cpu()
+    t_e2e = time.perf_counter() - t0
+    t_e2e = allmax(t_e2e)
+
+    # ---- value: device-resident frames, CUDA events on the library stream
+    lib = N.lib()
+    ext = torch.cuda.ExternalStream(ctx.stream)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    N.check(lib.riann_timing_enable(ctx.h, 1))
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(ext)
+    for k in range(K):
+        f = dev_frames[k]
+        st = N.FrameStatsC()
+        N.check(lib.riann_process_frame(
+            ctx.h, C.c_void_p(f.data_ptr()), f.shape[0], f.shape[1], f.shape[2] if f.dim() == 3 else 1, y0,
+            None, 0, stream.t + 1, 20, 0.25, 8, N.F_DEVICE_PTRS | N.F_TEMPORAL | N.F_KEEP_UNITS,
+            None, None, C.byref(st)))
+        stream.t += 1
+        stats.append(st)
+    ev1.record(ext)
+    ev1.synchronize()
+    barrier()
+    ms_value = allmax(ev0.elapsed_time(ev1) / K)
+    ms3 = (C.c_double * 3)()
+    nfr, nl = C.c_uint64(0), C.c_uint64(0)
+    N.check(lib.riann_timing_read(ctx.h, ms3, C.byref(nfr), C.byref(nl)))
+    N.check(lib.riann_timing_enable(ctx.h, 0))
+    clk = clocks.stop()
+
+    q_total = cfg.queries
+    value = q_total * K / (ms_value / 1e3 * K)
+    e2e = q_total * K / t_e2e
+
+    # roofline of the query kernel (K2) over the timed frames
+    from paper_1508_07953_b200.engine import FrameStats
+
+    fstats = [FrameStats(int(s.total_rings), int(s.total_distance_evals), 0.0, 0.0, int(s.queries),
+                         first_ring_total=int(s.sum_first_ring)) for s in stats]
+    bytes_k2 = allsum(sum(algorithmic_bytes(s, cfg.dim, cfg.n_refs) for s in fstats))
+    k2_ms = allmax(ms3[1])  # summed over K frames
+    achieved = bytes_k2 / (k2_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peaks()
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "query_kernel_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        if tj.get("config") == cfg.name:
+            traffic = tj.get("dram_bytes_per_frame")
+    evals = sum(s.total_distance_evals for s in fstats) / max(1, sum(s.queries for s in fstats))
+
+    # ---- CPU baseline: oracle on a sample of the last e2e frame (rank 0, N=1)
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        from oracle import oracle as O
+
+        om = O.LazyOracleModel(refs) if cfg.n_refs > 8192 else O.OracleModel.build(refs)
+        pos = sample_positions(gw, 0, gh, a.cpu_positions)
+        fi = Wm + K - 1
+        prev_idx = fields[fi - 1][0].ravel()[pos]
+        units = sample_units(host[fi].numpy(), cfg, pos, gw)
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        r = O.query_positions(om, units, prev_idx, pos, gw, 0, fi + 1, nthreads=threads)
+        t_cold = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r = O.query_positions(om, units, prev_idx, pos, gw, 0, fi + 1, nthreads=threads)
+        t_warm = time.perf_counter() - t0
+        gi, gd = fields[fi][0].ravel()[pos], fields[fi][1].ravel()[pos]
+        parity = {"positions": int(len(pos)), "frame": fi + 1,
+                  "idx_equal_frac": float(np.mean(gi == r["idx"])),
+                  "dist_bit_equal_frac": float(np.mean(gd.view(np.uint64) == r["dist"].view(np.uint64))),
+                  "max_rel_dist_err": float(np.max(np.abs(gd - r["dist"]) / np.maximum(r["dist"], 1e-300)))}
+        cpu = {"value": len(pos) / t_warm, "unit": "query patches/s", "cores": threads, "kind": "port",
+               "sample": f"{len(pos)} stratified positions of frame {fi + 1} ({cfg.name}), GPU prev field; "
+                         f"C port of search.py:83-151 (oracle/), table rows built lazily before timing "
+                         f"(cold pass {t_cold:.1f}s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "query patches/sec per ANNF (1080p RGB, 8x8x3 patches, n=65536)",
+            "value": value, "unit": "query patches/s", "n_gpus": world, "steps": K, "warmup": Wm,
+            "ms_per_step": ms_value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded blurred-noise clip and reference crops with BASELINE config-3 shape)",
+            "config": {"workload": f"{cfg.name}: {cfg.width}x{cfg.height}x{cfg.channels}, 8x8 patches, "
+                                   f"n={cfg.n_refs}, L=20 alpha=0.25 max_rings=8",
+                       "queries_per_frame": q_total, "bands": world, "frames_per_s": 1e3 / ms_value,
+                       "evals_per_query": evals,
+                       "l2": "inputs larger than L2 (34 GB sorted tables, 1.6 GB unit rows per frame); "
+                             "no flush", "table_build_s": t_tables, "data_gen_s": t_data},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "query_kernel<192>", "kernel_ms_per_frame": k2_ms / K,
+                         "units_kernel_ms_per_frame": allmax(ms3[0]) / K},
+            "cpu_baseline": cpu,
+            "parity": parity,
+            "e2e": {"value": e2e, "unit": "query patches/s", "ms_per_step": 1e3 * t_e2e / K,
+                    "h2d_bytes_per_step": int(host[0].numel() * 4 * world),
+                    "d2h_bytes_per_step": int(q_total * 12)},
+            "gpu_launches": int(nl.value) * world,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -105,6 +105,12 @@ int riann_process_frame(riann_ctx *ctx, const float *frame, int H, int W, int C,
 /* Upload prev units (rows, dim) for the next RIANN_F_TEMPORAL frame
  * (process_frame's prev_unit argument, engine.py:163-171). */
 int riann_set_prev_units(riann_ctx *ctx, const float *units, int64_t rows, int dim);
+/* Per-kernel CUDA-event timing of riann_process_frame on the ctx stream:
+ * enable (on=1) clears the accumulators; read synchronises and returns the
+ * summed milliseconds of [K1 units, K2 query, pairwise reduction], the number
+ * of frames and of kernel launches since enable. */
+int riann_timing_enable(riann_ctx *ctx, int on);
+int riann_timing_read(riann_ctx *ctx, double *ms3, uint64_t *frames, uint64_t *launches);
 /* Read back the device-resident field of the last frame. */
 int riann_field_get(riann_ctx *ctx, int32_t *idx, double *dist, int64_t count);
 

@@ -56,6 +56,10 @@ def _L():
         lib.rno_temporal_change.argtypes = [P, P, i64, i32]
         lib.rno_temporal_change.restype = dbl
         lib.rno_exact_nn_batch.argtypes = [P, i64, i32, P, i64, i32, P, P]
+        lib.rno_lazy_tables_create.argtypes = [i64, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
+        lib.rno_lazy_tables_free.argtypes = [i64, P, P, P]
+        lib.rno_lazy_rows_ready.argtypes = [P, i64]
+        lib.rno_lazy_rows_ready.restype = i64
         _lib = lib
     return _lib
 
@@ -71,6 +75,7 @@ class _Model(C.Structure):
         ("sorted_idx", C.c_void_p),
         ("n", C.c_int64),
         ("dim", C.c_int),
+        ("row_state", C.c_void_p),
     ]
 
 
@@ -205,7 +210,7 @@ class OracleModel:
         self.sorted_dist = np.ascontiguousarray(self.sorted_dist, dtype=np.float32)
         self.sorted_idx = np.ascontiguousarray(self.sorted_idx, dtype=np.int32)
         self._s = _Model(self.refs.ctypes.data, self.sorted_dist.ctypes.data,
-                         self.sorted_idx.ctypes.data, self.refs.shape[0], self.refs.shape[1])
+                         self.sorted_idx.ctypes.data, self.refs.shape[0], self.refs.shape[1], None)
 
     @property
     def n(self):
@@ -219,6 +224,42 @@ class OracleModel:
     def build(cls, refs, nthreads=None):
         sd, si = sorted_lists(refs, nthreads=nthreads)
         return cls(refs, sd, si)
+
+    @classmethod
+    def lazy(cls, refs):
+        """Tables built row by row on first use (for n where the full
+        (n, n) build is impractical on the CPU, e.g. config 3)."""
+        return LazyOracleModel(refs)
+
+
+class LazyOracleModel:
+    """OracleModel whose sorted-table rows are computed on demand."""
+
+    def __init__(self, refs):
+        self.refs = np.ascontiguousarray(refs, dtype=np.float32)
+        n, dim = self.refs.shape
+        sd, si, st = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        if _L().rno_lazy_tables_create(n, C.byref(sd), C.byref(si), C.byref(st)):
+            raise MemoryError("cannot map lazy tables")
+        self._ptrs = (sd.value, si.value, st.value)
+        self._s = _Model(self.refs.ctypes.data, sd.value, si.value, n, dim, st.value)
+
+    @property
+    def n(self):
+        return self.refs.shape[0]
+
+    @property
+    def dim(self):
+        return self.refs.shape[1]
+
+    def rows_ready(self) -> int:
+        return int(_L().rno_lazy_rows_ready(self._ptrs[2], self.n))
+
+    def __del__(self):
+        try:
+            _L().rno_lazy_tables_free(self.n, *self._ptrs)
+        except Exception:
+            pass
 
 
 def ring_window(model: OracleModel, anchor: int, d: float, eps: float):

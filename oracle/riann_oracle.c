@@ -7,10 +7,13 @@
  */
 #include "riann_oracle.h"
 
+#define _GNU_SOURCE
 #include <math.h>
 #include <pthread.h>
+#include <sched.h>
 #include <stdlib.h>
 #include <string.h>
+#include <sys/mman.h>
 
 /* ------------------------------------------------------------------------ */
 /* numpy float64 pairwise summation (the reduction np.sum applies along a
@@ -207,38 +210,40 @@ static void sorted_fr(void *p)
     free(k);
 }
 
+/* one row of compute_sorted_lists (model.py:177-188) */
+static void build_row(const float *refs, int64_t n, int dim, int64_t i, float *dr, int32_t *ir,
+                      double *tmp, uint64_t *keys)
+{
+    const float *qi = refs + i * dim;
+    for (int64_t j = 0; j < n; j++) {
+        float v = (float)sq_dist(qi, refs + j * dim, dim, tmp);
+        uint32_t bits;
+        memcpy(&bits, &v, 4);
+        /* non-negative floats order like their bit patterns; the index in
+         * the low word makes the order the stable argsort's */
+        keys[j] = ((uint64_t)bits << 32) | (uint64_t)j;
+    }
+    qsort(keys, (size_t)n, sizeof(uint64_t), cmp_u64);
+    int64_t self = 0;
+    while ((int64_t)(uint32_t)keys[self] != i) self++;
+    if (self != 0) { /* duplicates of i sort ahead of it: self goes first */
+        uint64_t sk = keys[self];
+        memmove(keys + 1, keys, sizeof(uint64_t) * (size_t)self);
+        keys[0] = sk;
+    }
+    for (int64_t j = 0; j < n; j++) {
+        uint32_t bits = (uint32_t)(keys[j] >> 32);
+        memcpy(&dr[j], &bits, 4);
+        ir[j] = (int32_t)(uint32_t)keys[j];
+    }
+}
+
 static void sorted_rows(void *c, int64_t lo, int64_t hi, void *scr)
 {
     sorted_ctx *s = (sorted_ctx *)c;
     sorted_scratch *k = (sorted_scratch *)scr;
-    int64_t n = s->n;
-    for (int64_t r = lo; r < hi; r++) {
-        int64_t i = s->row0 + r;
-        const float *qi = s->refs + i * s->dim;
-        for (int64_t j = 0; j < n; j++) {
-            float v = (float)sq_dist(qi, s->refs + j * s->dim, s->dim, k->tmp);
-            uint32_t bits;
-            memcpy(&bits, &v, 4);
-            /* non-negative floats order like their bit patterns; the index in
-             * the low word makes the order the stable argsort's */
-            k->keys[j] = ((uint64_t)bits << 32) | (uint64_t)j;
-        }
-        qsort(k->keys, (size_t)n, sizeof(uint64_t), cmp_u64);
-        int64_t self = 0;
-        while ((int64_t)(uint32_t)k->keys[self] != i) self++;
-        if (self != 0) { /* duplicates of i sort ahead of it: self goes first */
-            uint64_t sk = k->keys[self];
-            memmove(k->keys + 1, k->keys, sizeof(uint64_t) * (size_t)self);
-            k->keys[0] = sk;
-        }
-        float *dr = s->sdist + r * n;
-        int32_t *ir = s->sidx + r * n;
-        for (int64_t j = 0; j < n; j++) {
-            uint32_t bits = (uint32_t)(k->keys[j] >> 32);
-            memcpy(&dr[j], &bits, 4);
-            ir[j] = (int32_t)(uint32_t)k->keys[j];
-        }
-    }
+    for (int64_t r = lo; r < hi; r++)
+        build_row(s->refs, s->n, s->dim, s->row0 + r, s->sdist + r * s->n, s->sidx + r * s->n, k->tmp, k->keys);
 }
 
 int rno_sorted_lists(const float *refs, int64_t n, int dim, int64_t row0,
@@ -399,6 +404,7 @@ typedef struct {
     unsigned char *mark;
     double *dtmp;
     double *dists;
+    uint64_t *keys; /* lazy row builds */
 } query_scratch;
 
 static int cmp_i32(const void *a, const void *b)
@@ -417,6 +423,7 @@ static void *query_mk_n(int64_t n, int dim)
     s->mark = (unsigned char *)calloc((size_t)n, 1);
     s->dtmp = (double *)malloc(sizeof(double) * (size_t)dim);
     s->dists = (double *)malloc(sizeof(double) * (size_t)(n + 1));
+    s->keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n);
     return s;
 }
 
@@ -430,7 +437,54 @@ static void query_fr(void *p)
     free(s->mark);
     free(s->dtmp);
     free(s->dists);
+    free(s->keys);
     free(s);
+}
+
+static void ensure_row(const rno_model *m, int64_t a, query_scratch *s)
+{
+    if (!m->row_state) return;
+    unsigned char *st = m->row_state + a;
+    if (__atomic_load_n(st, __ATOMIC_ACQUIRE) == 2) return;
+    unsigned char expect = 0;
+    if (__atomic_compare_exchange_n(st, &expect, 1, 0, __ATOMIC_ACQ_REL, __ATOMIC_ACQUIRE)) {
+        build_row(m->refs, m->n, m->dim, a, (float *)m->sorted_dist + a * m->n,
+                  (int32_t *)m->sorted_idx + a * m->n, s->dtmp, s->keys);
+        __atomic_store_n(st, 2, __ATOMIC_RELEASE);
+    } else {
+        while (__atomic_load_n(st, __ATOMIC_ACQUIRE) != 2) sched_yield();
+    }
+}
+
+int rno_lazy_tables_create(int64_t n, float **sdist, int32_t **sidx, unsigned char **state)
+{
+    size_t bytes = (size_t)n * (size_t)n * 4;
+    void *a = mmap(NULL, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (a == MAP_FAILED) return -1;
+    void *b = mmap(NULL, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (b == MAP_FAILED) {
+        munmap(a, bytes);
+        return -1;
+    }
+    *sdist = (float *)a;
+    *sidx = (int32_t *)b;
+    *state = (unsigned char *)calloc((size_t)n, 1);
+    return 0;
+}
+
+void rno_lazy_tables_free(int64_t n, float *sdist, int32_t *sidx, unsigned char *state)
+{
+    size_t bytes = (size_t)n * (size_t)n * 4;
+    if (sdist) munmap(sdist, bytes);
+    if (sidx) munmap(sidx, bytes);
+    free(state);
+}
+
+int64_t rno_lazy_rows_ready(const unsigned char *state, int64_t n)
+{
+    int64_t c = 0;
+    for (int64_t i = 0; i < n; i++) c += state[i] == 2;
+    return c;
 }
 
 /* search.py:83-151 */
@@ -442,6 +496,7 @@ static int query_impl(const rno_model *m, const float *q, int32_t prev, int L,
     int64_t n = m->n;
     int dim = m->dim;
     if (prev < 0 || prev >= n) return -2;
+    ensure_row(m, prev, s);
     double d = sq_dist(q, m->refs + (int64_t)prev * dim, dim, s->dtmp);
     int64_t evals = 1;
     int64_t lo, hi;
@@ -472,6 +527,7 @@ static int query_impl(const rno_model *m, const float *q, int32_t prev, int L,
         s->mark[a] |= 2;
         double da = sq_dist(q, m->refs + (int64_t)a * dim, dim, s->dtmp);
         evals++;
+        ensure_row(m, a, s);
         rno_ring_window(m->sorted_dist + (int64_t)a * n, n, da, alpha * da, &lo, &hi);
         const int32_t *ring = m->sorted_idx + (int64_t)a * n;
         for (int64_t i = lo; i < hi; i++) s->mark[ring[i]] |= 1;

@@ -81,7 +81,17 @@ typedef struct {
     const int32_t *sorted_idx;/* (n, n) */
     int64_t n;
     int dim;
+    /* NULL: tables complete.  Otherwise per-row state (0 absent, 1 building,
+     * 2 ready): rows are built on first use (model.py:162-189 per row), so a
+     * sampled query run touches only the rows it needs. */
+    unsigned char *row_state;
 } rno_model;
+
+/* Lazily backed (n, n) tables for rno_model.row_state mode (anonymous
+ * MAP_NORESERVE mappings: untouched rows cost no memory). */
+int rno_lazy_tables_create(int64_t n, float **sdist, int32_t **sidx, unsigned char **state);
+void rno_lazy_tables_free(int64_t n, float *sdist, int32_t *sidx, unsigned char *state);
+int64_t rno_lazy_rows_ready(const unsigned char *state, int64_t n);
 
 typedef struct {
     int32_t match_index;

@@ -11,6 +11,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <array>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -179,6 +180,24 @@ struct riann_ctx {
     int cur_fld = 0;
     int64_t field_count = -1;
     PwTree tree;
+    // per-kernel event timing of the frame path (riann_timing_*)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::array<cudaEvent_t, 4>> ev_pending;
+    double t_ms[3] = {0, 0, 0};
+    uint64_t t_frames = 0, launches = 0;
+
+    cudaEvent_t ev()
+    {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
 
     int use()
     {
@@ -440,6 +459,9 @@ int riann_ctx_destroy(riann_ctx *c)
                       &c->tree.leaf_start, &c->tree.leaf_len, &c->tree.leaf_node, &c->tree.level_off,
                       &c->tree.inner, &c->tree.left, &c->tree.right, &c->tree.node_val};
     for (DevBuf *b : bufs) b->release();
+    for (auto &a : c->ev_pending)
+        for (auto e : a) cudaEventDestroy(e);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     delete c;
     return 0;
@@ -636,6 +658,12 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
     const int us = c->cur_units;
     RET(c->units[us].ensure((size_t)Q * c->dim * 4));
     if (temporal) RET(c->tc.ensure((size_t)Q * 8));
+    std::array<cudaEvent_t, 4> evs = {nullptr, nullptr, nullptr, nullptr};
+    if (c->timing) {
+        for (auto &e : evs) e = c->ev();
+        CK(cudaEventRecord(evs[0], c->stream));
+    }
+    c->launches += 1;
     RET(launch_units(c, d_frame, H, W, C, c->units[us].as<float>(), nullptr,
                      temporal ? c->units[us ^ 1].as<float>() : nullptr, temporal ? c->tc.as<double>() : nullptr));
     // K2: queries
@@ -664,7 +692,12 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
     P.out_dist = d_dist;
     P.stats = c->stats.as<unsigned long long>();
     P.err = c->err.as<int>();
-    if (Q > 0) RET(launch_query(c, P));
+    if (c->timing) CK(cudaEventRecord(evs[1], c->stream));
+    if (Q > 0) {
+        RET(launch_query(c, P));
+        c->launches += 1;
+    }
+    if (c->timing) CK(cudaEventRecord(evs[2], c->stream));
     if (temporal && Q > 0) {
         RET(c->tree.build(Q));
         rb::PwTreeParams T;
@@ -682,6 +715,11 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         T.out = c->tc_sum.as<double>();
         rb::pw_tree_kernel<<<1, 1024, 0, c->stream>>>(T);
         CK(cudaGetLastError());
+        c->launches += 1;
+    }
+    if (c->timing) {
+        CK(cudaEventRecord(evs[3], c->stream));
+        c->ev_pending.push_back(evs);
     }
     if (!dev) {
         if (out_idx) CK(cudaMemcpyAsync(out_idx, d_idx, (size_t)Q * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -712,6 +750,43 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         stats->queries = (uint64_t)Q;
         stats->temporal_change = tcv;
     }
+    return 0;
+}
+
+int riann_timing_enable(riann_ctx *c, int on)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    RET(c->use());
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto &a : c->ev_pending)
+        for (auto e : a) c->ev_pool.push_back(e);
+    c->ev_pending.clear();
+    c->timing = on != 0;
+    c->t_ms[0] = c->t_ms[1] = c->t_ms[2] = 0.0;
+    c->t_frames = 0;
+    c->launches = 0;
+    return 0;
+}
+
+int riann_timing_read(riann_ctx *c, double *ms3, uint64_t *frames, uint64_t *launches)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    RET(c->use());
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto &a : c->ev_pending) {
+        for (int k = 0; k < 3; k++) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, a[k], a[k + 1]));
+            c->t_ms[k] += ms;
+        }
+        for (auto e : a) c->ev_pool.push_back(e);
+        c->t_frames++;
+    }
+    c->ev_pending.clear();
+    if (ms3)
+        for (int k = 0; k < 3; k++) ms3[k] = c->t_ms[k];
+    if (frames) *frames = c->t_frames;
+    if (launches) *launches = c->launches;
     return 0;
 }
 

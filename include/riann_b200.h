@@ -58,6 +58,8 @@ typedef struct {
     uint64_t sum_first_ring;   /* sum |S_1|: roofline byte count */
     uint64_t queries;
     double temporal_change;
+    uint64_t sum_ring_tests;   /* sum over rings of |S| membership lookups */
+    uint64_t sum_exact_evals;  /* FP64 distances actually evaluated (screening survivors) */
 } riann_frame_stats;
 
 int riann_abi_version(void);

@@ -31,6 +31,8 @@ class FrameStatsC(C.Structure):
         ("sum_first_ring", C.c_uint64),
         ("queries", C.c_uint64),
         ("temporal_change", C.c_double),
+        ("sum_ring_tests", C.c_uint64),
+        ("sum_exact_evals", C.c_uint64),
     ]
 
 

@@ -76,7 +76,8 @@ class BandStream:
         stats = FrameStats(int(st.total_rings), int(st.total_distance_evals),
                            float(int(st.sum_cand_final)) / max(q, 1),
                            float(st.temporal_change) if self.t > 1 else 0.0, q,
-                           first_ring_total=int(st.sum_first_ring), cand_total=int(st.sum_cand_final))
+                           first_ring_total=int(st.sum_first_ring), cand_total=int(st.sum_cand_final),
+                           ring_tests_total=int(st.sum_ring_tests), exact_evals_total=int(st.sum_exact_evals))
         return idx, dist, stats
 
 

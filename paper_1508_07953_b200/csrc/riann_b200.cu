@@ -11,6 +11,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <array>
 #include <cstring>
 #include <string>
@@ -170,7 +171,8 @@ struct riann_ctx {
     int64_t n = 0;
     int dim = 0, pw = 0, ph = 0, C = 1;
     bool tables = false;
-    DevBuf refs, sdist, sidx;
+    bool idx16 = false;  // sorted index table stored as uint16 (n <= 65536)
+    DevBuf refs, refs16, err16, sdist, sidx, dmat;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -206,7 +208,7 @@ struct riann_ctx {
     }
     uint64_t bytes() const
     {
-        uint64_t b = refs.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
+        uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
                      fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap;
         return b;
     }
@@ -214,46 +216,48 @@ struct riann_ctx {
 
 namespace {
 
-int bitmap_words(int64_t n)
-{
-    int64_t w = (n + 31) / 32;
-    w = (w + 31) / 32 * 32;
-    return (int)(w < 32 ? 32 : w);
-}
-
-template <int D>
+template <int D, class IdxT>
 int launch_query_t(riann_ctx *c, rb::QueryParams &P)
 {
-    const size_t per_warp = (size_t)(P.nw + rb::HIT_CAP) * 4;
-    int wpb = 8;
-    while (wpb > 1 && per_warp * wpb > (size_t)c->smem_optin) wpb--;
-    if (per_warp * wpb > (size_t)c->smem_optin)
-        return fail(RIANN_E_CAPACITY, "model n=%lld needs %zu B shared memory per warp", (long long)c->n, per_warp);
+    const size_t per_warp = (size_t)rb::K2_SMEM_WORDS * 4;
+    const int wpb = 8;
     const size_t smem = per_warp * wpb;
-    CK(cudaFuncSetAttribute(rb::query_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = rb::query_kernel<D, IdxT>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, rb::query_kernel<D>, wpb * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
     if (bps < 1) bps = 1;
     int64_t blocks = (int64_t)c->sms * bps;
     int64_t need = (P.Q + wpb - 1) / wpb;
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    RET(c->overflow.ensure((size_t)blocks * wpb * (size_t)c->n * 4));
-    P.overflow = c->overflow.as<int32_t>();
-    rb::query_kernel<D><<<(unsigned)blocks, wpb * 32, smem, c->stream>>>(P);
+    RET(c->overflow.ensure((size_t)blocks * wpb * 2 * (size_t)c->n * 4));
+    P.overflow = c->overflow.as<uint32_t>();
+    kern<<<(unsigned)blocks, wpb * 32, smem, c->stream>>>(P);
     CK(cudaGetLastError());
     return 0;
 }
 
+template <class IdxT>
+int launch_query_i(riann_ctx *c, rb::QueryParams &P)
+{
+    switch (c->dim) {
+    case 16: return launch_query_t<16, IdxT>(c, P);
+    case 64: return launch_query_t<64, IdxT>(c, P);
+    case 192: return launch_query_t<192, IdxT>(c, P);
+    default: return launch_query_t<0, IdxT>(c, P);
+    }
+}
+
 int launch_query(riann_ctx *c, rb::QueryParams &P)
 {
-    P.nw = bitmap_words(c->n);
-    switch (c->dim) {
-    case 16: return launch_query_t<16>(c, P);
-    case 64: return launch_query_t<64>(c, P);
-    case 192: return launch_query_t<192>(c, P);
-    default: return launch_query_t<0>(c, P);
-    }
+    P.refs16 = c->refs16.as<__half>();
+    P.err16 = c->err16.as<float>();
+    P.dmat = c->dmat.as<float>();
+    int bits = 1;
+    while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
+    P.passes = (bits + 7) / 8;
+    return c->idx16 ? launch_query_i<uint16_t>(c, P) : launch_query_i<int32_t>(c, P);
 }
 
 int check_model(riann_ctx *c, bool need_tables)
@@ -452,7 +456,7 @@ int riann_ctx_destroy(riann_ctx *c)
     if (!c) return 0;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    DevBuf *bufs[] = {&c->refs, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
+    DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
                       &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,
@@ -493,9 +497,15 @@ int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, in
     CK(cudaStreamSynchronize(c->stream));
     c->sdist.release();
     c->sidx.release();
+    c->dmat.release();
     c->tables = false;
     RET(c->refs.ensure((size_t)n * dim * 4));
     CK(cudaMemcpyAsync(c->refs.p, refs, (size_t)n * dim * 4, cudaMemcpyHostToDevice, c->stream));
+    RET(c->refs16.ensure((size_t)n * dim * 2));
+    RET(c->err16.ensure((size_t)n * 4));
+    rb::refs16_kernel<<<(unsigned)((n + 127) / 128), 128, 0, c->stream>>>(c->refs.as<float>(), n, dim,
+                                                                          c->refs16.as<__half>(), c->err16.as<float>());
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     c->n = n;
     c->dim = dim;
@@ -511,12 +521,37 @@ int riann_model_set_tables(riann_ctx *c, const float *sd, const int32_t *si)
 {
     RET(check_model(c, false));
     RET(c->use());
-    const size_t bytes = (size_t)c->n * c->n * 4;
-    RET(c->sdist.ensure(bytes));
-    RET(c->sidx.ensure(bytes));
-    CK(cudaMemcpyAsync(c->sdist.p, sd, bytes, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->sidx.p, si, bytes, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    const int64_t n = c->n;
+    const size_t cnt = (size_t)n * n;
+    c->idx16 = n <= 65536;
+    RET(c->sdist.ensure(cnt * 4));
+    RET(c->sidx.ensure(cnt * (c->idx16 ? 2 : 4)));
+    RET(c->dmat.ensure(cnt * 4));
+    CK(cudaMemcpyAsync(c->sdist.p, sd, cnt * 4, cudaMemcpyHostToDevice, c->stream));
+    // index rows in chunks through a staging buffer (narrowed to u16 when possible)
+    const int64_t chunk_rows = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)n * 4)));
+    DevBuf stage;
+    RET(stage.ensure((size_t)std::min<int64_t>(chunk_rows, n) * n * 4));
+    for (int64_t r0 = 0; r0 < n; r0 += chunk_rows) {
+        const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
+        const size_t m = (size_t)rows * n;
+        CK(cudaMemcpyAsync(stage.p, si + (size_t)r0 * n, m * 4, cudaMemcpyHostToDevice, c->stream));
+        const unsigned blocks = (unsigned)((m + 255) / 256);
+        if (c->idx16) {
+            uint16_t *dst = c->sidx.as<uint16_t>() + (size_t)r0 * n;
+            rb::narrow_u16_kernel<<<blocks, 256, 0, c->stream>>>(stage.as<int32_t>(), dst, (int64_t)m);
+            rb::dmat_scatter_kernel<uint16_t><<<blocks, 256, 0, c->stream>>>(
+                c->sdist.as<float>() + (size_t)r0 * n, dst, n, rows, c->dmat.as<float>() + (size_t)r0 * n);
+        } else {
+            int32_t *dst = c->sidx.as<int32_t>() + (size_t)r0 * n;
+            CK(cudaMemcpyAsync(dst, stage.p, m * 4, cudaMemcpyDeviceToDevice, c->stream));
+            rb::dmat_scatter_kernel<int32_t><<<blocks, 256, 0, c->stream>>>(
+                c->sdist.as<float>() + (size_t)r0 * n, dst, n, rows, c->dmat.as<float>() + (size_t)r0 * n);
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    stage.release();
     c->tables = true;
     return 0;
 }
@@ -526,17 +561,20 @@ int riann_model_build_tables(riann_ctx *c)
     RET(check_model(c, false));
     RET(c->use());
     const int64_t n = c->n;
-    const size_t tbytes = (size_t)n * n * 4;
-    RET(c->sdist.ensure(tbytes));
-    RET(c->sidx.ensure(tbytes));
+    const size_t tcnt = (size_t)n * n;
+    c->idx16 = n <= 65536;
+    RET(c->sdist.ensure(tcnt * 4));
+    RET(c->sidx.ensure(tcnt * (c->idx16 ? 2 : 4)));
+    RET(c->dmat.ensure(tcnt * 4));
     // row batches bounded by ~1 GiB of unsorted keys+values
     int64_t rb_rows = (int64_t)((1ull << 30) / ((size_t)n * 8));
     if (rb_rows < 1) rb_rows = 1;
     if (rb_rows > n) rb_rows = n;
     if ((int64_t)rb_rows * n > 0x7fffffffLL) rb_rows = 0x7fffffffLL / n;
-    RET(c->keys.ensure((size_t)rb_rows * n * 8));
+    RET(c->keys.ensure((size_t)rb_rows * n * 12));
     uint32_t *keys_in = c->keys.as<uint32_t>();
     int32_t *vals_in = reinterpret_cast<int32_t *>(keys_in + (size_t)rb_rows * n);
+    int32_t *vals_out = vals_in + (size_t)rb_rows * n;
     // segment offsets r*n
     std::vector<int> offs(rb_rows + 1);
     for (int64_t r = 0; r <= rb_rows; r++) offs[r] = (int)(r * n);
@@ -551,7 +589,7 @@ int riann_model_build_tables(riann_ctx *c)
     RET(temp.ensure(temp_bytes));
     for (int64_t r0 = 0; r0 < n; r0 += rb_rows) {
         const int64_t rows = (r0 + rb_rows <= n) ? rb_rows : n - r0;
-        const unsigned blocks = (unsigned)((rows + 7) / 8 < (int64_t)c->sms * 8 ? (rows + 7) / 8 : (int64_t)c->sms * 8);
+        const unsigned blocks = (unsigned)std::min<int64_t>((rows + 7) / 8, (int64_t)c->sms * 8);
         switch (c->dim) {
         case 16: rb::table_keys_kernel<16><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
         case 64: rb::table_keys_kernel<64><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
@@ -559,13 +597,21 @@ int riann_model_build_tables(riann_ctx *c)
         default: rb::table_keys_kernel<0><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
         }
         CK(cudaGetLastError());
+        // index-ordered distances are the unsorted keys
+        CK(cudaMemcpyAsync(c->dmat.as<float>() + (size_t)r0 * n, keys_in, (size_t)rows * n * 4,
+                           cudaMemcpyDeviceToDevice, c->stream));
         uint32_t *kout = reinterpret_cast<uint32_t *>(c->sdist.as<float>() + (size_t)r0 * n);
-        int32_t *vout = c->sidx.as<int32_t>() + (size_t)r0 * n;
+        int32_t *vout = c->idx16 ? vals_out : c->sidx.as<int32_t>() + (size_t)r0 * n;
         CK(cub::DeviceSegmentedRadixSort::SortPairs(temp.p, temp_bytes, keys_in, kout, vals_in, vout,
                                                      (int)(rows * n), (int)rows, d_off.as<int>(),
                                                      d_off.as<int>() + 1, 0, 32, c->stream));
         rb::self_first_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, c->stream>>>(kout, vout, n, r0, rows);
         CK(cudaGetLastError());
+        if (c->idx16) {
+            rb::narrow_u16_kernel<<<(unsigned)((rows * n + 255) / 256), 256, 0, c->stream>>>(
+                vout, c->sidx.as<uint16_t>() + (size_t)r0 * n, rows * n);
+            CK(cudaGetLastError());
+        }
     }
     CK(cudaStreamSynchronize(c->stream));
     temp.release();
@@ -580,9 +626,26 @@ int riann_model_get_tables(riann_ctx *c, int64_t row0, int64_t rows, float *sd, 
     RET(check_model(c, true));
     if (row0 < 0 || rows < 0 || row0 + rows > c->n) return fail(RIANN_E_INDEX, "rows out of range");
     RET(c->use());
-    const size_t off = (size_t)row0 * c->n, cnt = (size_t)rows * c->n;
+    const int64_t n = c->n;
+    const size_t off = (size_t)row0 * n, cnt = (size_t)rows * n;
     if (sd) CK(cudaMemcpyAsync(sd, c->sdist.as<float>() + off, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
-    if (si) CK(cudaMemcpyAsync(si, c->sidx.as<int32_t>() + off, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (si) {
+        if (!c->idx16) {
+            CK(cudaMemcpyAsync(si, c->sidx.as<int32_t>() + off, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
+        } else {
+            const int64_t chunk = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)n * 4)));
+            DevBuf stage;
+            RET(stage.ensure((size_t)std::min<int64_t>(chunk, rows) * n * 4));
+            for (int64_t r = 0; r < rows; r += chunk) {
+                const int64_t m = std::min<int64_t>(chunk, rows - r) * n;
+                rb::widen_u16_kernel<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(
+                    c->sidx.as<uint16_t>() + off + (size_t)r * n, stage.as<int32_t>(), m);
+                CK(cudaGetLastError());
+                CK(cudaMemcpyAsync(si + (size_t)r * n, stage.p, (size_t)m * 4, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+            }
+        }
+    }
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -667,13 +730,13 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
     RET(launch_units(c, d_frame, H, W, C, c->units[us].as<float>(), nullptr,
                      temporal ? c->units[us ^ 1].as<float>() : nullptr, temporal ? c->tc.as<double>() : nullptr));
     // K2: queries
-    CK(cudaMemsetAsync(c->stats.p, 0, 32, c->stream));
+    CK(cudaMemsetAsync(c->stats.p, 0, 48, c->stream));
     CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
     rb::QueryParams P;
     memset(&P, 0, sizeof P);
     P.refs = c->refs.as<float>();
     P.sdist = c->sdist.as<float>();
-    P.sidx = c->sidx.as<int32_t>();
+    P.sidx = c->sidx.p;
     P.n = c->n;
     P.dim = c->dim;
     P.units = c->units[us].as<float>();
@@ -737,9 +800,9 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         c->prev_units_rows = Q;
     }
     if ((flags & RIANN_F_ASYNC) && dev) return 0;
-    unsigned long long hs[4] = {0, 0, 0, 0};
+    unsigned long long hs[6] = {0, 0, 0, 0, 0, 0};
     double tcv = 0.0;
-    CK(cudaMemcpyAsync(hs, c->stats.p, 32, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(hs, c->stats.p, 48, cudaMemcpyDeviceToHost, c->stream));
     if (temporal && Q > 0) CK(cudaMemcpyAsync(&tcv, c->tc_sum.p, 8, cudaMemcpyDeviceToHost, c->stream));
     RET(check_err(c));
     if (stats) {
@@ -749,6 +812,8 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         stats->sum_first_ring = hs[3];
         stats->queries = (uint64_t)Q;
         stats->temporal_change = tcv;
+        stats->sum_ring_tests = hs[4];
+        stats->sum_exact_evals = hs[5];
     }
     return 0;
 }
@@ -930,9 +995,17 @@ int riann_ring_candidates(riann_ctx *c, int64_t anchor, double d, double eps, in
     CK(cudaStreamSynchronize(c->stream));
     *lo = h[0];
     *hi = h[1];
-    if (out && h[1] > h[0])
-        CK(cudaMemcpy(out, c->sidx.as<int32_t>() + (size_t)anchor * c->n + h[0], (size_t)(h[1] - h[0]) * 4,
-                      cudaMemcpyDeviceToHost));
+    if (out && h[1] > h[0]) {
+        const size_t m = (size_t)(h[1] - h[0]);
+        if (c->idx16) {
+            std::vector<uint16_t> tmp(m);
+            CK(cudaMemcpy(tmp.data(), c->sidx.as<uint16_t>() + (size_t)anchor * c->n + h[0], m * 2,
+                          cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < m; i++) out[i] = tmp[i];
+        } else {
+            CK(cudaMemcpy(out, c->sidx.as<int32_t>() + (size_t)anchor * c->n + h[0], m * 4, cudaMemcpyDeviceToHost));
+        }
+    }
     return 0;
 }
 
@@ -976,7 +1049,7 @@ int riann_query_batch(riann_ctx *c, const float *queries, const int32_t *prev, c
     memset(&P, 0, sizeof P);
     P.refs = c->refs.as<float>();
     P.sdist = c->sdist.as<float>();
-    P.sidx = c->sidx.as<int32_t>();
+    P.sidx = c->sidx.p;
     P.n = c->n;
     P.dim = c->dim;
     P.units = dq.as<float>();

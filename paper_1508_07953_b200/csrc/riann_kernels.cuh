@@ -10,11 +10,12 @@
 //   pw_tree_kernel         numpy pairwise sum over Q per-position values
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "riann_device.cuh"
 
 namespace rb {
 
-constexpr int HIT_CAP = 1024;  // per-warp shared hit list (u32 entries); overflow spills to global
 
 // ---------------------------------------------------------------------------
 // K1: one thread per grid position.  Frame (H, W, C) row-major; patch element
@@ -174,10 +175,27 @@ __global__ void __launch_bounds__(1024) pw_tree_kernel(PwTreeParams P)
 
 // ---------------------------------------------------------------------------
 // K2: riann_query, one warp per query, persistent grid.
+//
+// Per query (search.py:83-151):
+//   d_prev exact; first ring = window of the previous match's sorted row
+//   (17-ary warp binary search, search.py:77-79) enumerated from the u16/i32
+//   index table and radix-sorted ascending (np.sort, search.py:116) into the
+//   warp's candidate list S;
+//   rings: anchor = k-th element of S minus used anchors (numpy RNG), exact
+//   d_a, and membership of every j in S by one lookup in the index-ordered
+//   distance matrix dmat[a][j] (== the sorted table's value, so lv <= v <= hv
+//   is exactly the searchsorted window test) -- |S| reads instead of
+//   enumerating the anchor's window (~30% of n at config 3);
+//   final scan of S u {prev}: fp16-reference screening with a rigorous error
+//   bound, exact FP64 (numpy order) only for the candidates that can still be
+//   the first minimum.
 struct QueryParams {
     const float *refs;
-    const float *sdist;
-    const int32_t *sidx;
+    const __half *refs16;   // fp16 copy of refs (screening)
+    const float *err16;     // per row: upper bound of ||r - fp16(r)||
+    const float *sdist;     // sorted distance rows (n, n)
+    const void *sidx;       // sorted index rows (n, n): uint16 or int32
+    const float *dmat;      // index-ordered distance rows (n, n)
     int64_t n;
     int dim;
     const float *units;   // (Q, dim)
@@ -201,25 +219,24 @@ struct QueryParams {
     int64_t *out_first;
     int32_t *scanned;     // optional, stride n+1
     int64_t *scanned_len;
-    unsigned long long *stats;  // [4]: rings, evals, cand_final, first_ring
+    unsigned long long *stats;  // [6]: rings, evals, cand_final, first_ring, ring_tests, exact_evals
     int *err;
-    int32_t *overflow;    // per warp: n entries
-    int nw;               // bitmap words per warp (multiple of 32)
+    uint32_t *overflow;   // per warp: 2n entries (list spill)
+    int passes;           // radix passes for indices < n
 };
 
 enum { ERR_PREV_RANGE = 3, ERR_USED_OVERFLOW = 5 };
+constexpr int SCAP = 1024;  // per-warp shared list capacity (entries); beyond it lists spill to global
+constexpr int K2_SMEM_WORDS = 2 * SCAP + 256;
 
-struct WarpList {
+struct QList {
     uint32_t *sm;
-    int32_t *gl;
-    __device__ __forceinline__ void put(int pos, int v) const
+    uint32_t *gl;
+    __device__ __forceinline__ uint32_t get(int i) const { return i < SCAP ? sm[i] : gl[i - SCAP]; }
+    __device__ __forceinline__ void put(int i, uint32_t v) const
     {
-        if (pos < HIT_CAP) sm[pos] = (uint32_t)v;
-        else gl[pos - HIT_CAP] = v;
-    }
-    __device__ __forceinline__ int get(int pos) const
-    {
-        return pos < HIT_CAP ? (int)sm[pos] : gl[pos - HIT_CAP];
+        if (i < SCAP) sm[i] = v;
+        else gl[i - SCAP] = v;
     }
 };
 
@@ -263,244 +280,409 @@ __device__ __forceinline__ void ring_window(const float *__restrict__ row, int64
     hi = __shfl_sync(FULL, res, 16);
 }
 
-// k-th (0-based) set bit of the warp's bitmap (ascending order).
-__device__ __forceinline__ int rank_select(const uint32_t *bm, int nw, int k, int lane)
+// Stable LSD radix sort (8-bit digits) of list a[0..cnt) using b as buffer;
+// the sorted result ends in `a` (the lists are swapped per pass).
+__device__ __forceinline__ void warp_radix_sort(QList &a, QList &b, int cnt, int passes, uint32_t *hist, int lane)
 {
-    const int CH = nw >> 5;
-    const uint32_t *mine = bm + lane * CH;
-    int c = 0;
-    for (int w = 0; w < CH; w++) c += __popc(mine[w]);
-    int inc = warp_incl_scan(c, lane);
-    unsigned ball = __ballot_sync(FULL, k < inc);
-    int L = __ffs(ball) - 1;
-    int kk = k - __shfl_sync(FULL, inc - c, L);
-    const uint32_t *ch = bm + L * CH;
-    for (int base = 0; base < CH; base += 32) {
-        uint32_t w = (base + lane < CH) ? ch[base + lane] : 0u;
-        int pc = __popc(w);
-        int inc2 = warp_incl_scan(pc, lane);
-        int tot = __shfl_sync(FULL, inc2, 31);
-        if (kk < tot) {
-            unsigned b2 = __ballot_sync(FULL, kk < inc2);
-            int L2 = __ffs(b2) - 1;
-            int k2 = kk - __shfl_sync(FULL, inc2 - pc, L2);
-            uint32_t word = __shfl_sync(FULL, w, L2);
-            for (int i = 0; i < k2; i++) word &= word - 1;
-            return (L * CH + base + L2) * 32 + (__ffs(word) - 1);
+    for (int ps = 0; ps < passes; ps++) {
+        const int sh = 8 * ps;
+        for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+        __syncwarp();
+        for (int i = lane; i < cnt; i += 32) atomicAdd(&hist[(a.get(i) >> sh) & 255u], 1u);
+        __syncwarp();
+        uint32_t v[8], s = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            v[k] = hist[lane * 8 + k];
+            s += v[k];
         }
-        kk -= tot;
+        uint32_t run = (uint32_t)warp_incl_scan((int)s, lane) - s;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            hist[lane * 8 + k] = run;
+            run += v[k];
+        }
+        __syncwarp();
+        for (int base = 0; base < cnt; base += 32) {
+            const int i = base + lane;
+            const bool valid = i < cnt;
+            const uint32_t key = valid ? a.get(i) : 0u;
+            const uint32_t dg = valid ? ((key >> sh) & 255u) : 256u;
+            const unsigned m = __match_any_sync(FULL, dg);
+            const int rank = __popc(m & lanemask_lt());
+            const uint32_t bse = valid ? hist[dg] : 0u;
+            __syncwarp();
+            if (valid) b.put((int)bse + rank, key);
+            if (valid && rank == 0) hist[dg] = bse + (uint32_t)__popc(m);
+            __syncwarp();
+        }
+        QList t = a;
+        a = b;
+        b = t;
+        __threadfence_block();
+        __syncwarp();
     }
-    return -1;  // unreachable when k < popcount
 }
 
-__device__ __forceinline__ bool bit_test(const uint32_t *bm, int j)
+// first position in ascending list a[0..cnt) with value >= x (one lane)
+__device__ __forceinline__ int list_lower_bound(const QList &a, int cnt, uint32_t x)
 {
-    return (bm[j >> 5] >> (j & 31)) & 1u;
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a.get(mid) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
-// D > 0: compile-time dim with the warp-cooperative exact distance;
-// D == 0: runtime dim, one lane per distance.
+// fp16 screening layout (D in {64, 192}): 8 lanes per candidate, lane l8
+// owns elements m*64 + l8*8 + e (m < D/64, e < 8): one 16-byte load per m.
 template <int D>
-__global__ void __launch_bounds__(256) query_kernel(QueryParams P)
+struct Scr {
+    static constexpr bool on = (D == 64 || D == 192);
+    static constexpr int NV = D / 64;
+    static constexpr int PER = D / 8;
+};
+
+template <int D>
+__device__ __forceinline__ float approx_sq(const __half *__restrict__ row16, const float (&q)[Scr<D>::PER], int l8)
+{
+    const uint4 *p = reinterpret_cast<const uint4 *>(row16) + l8;
+    float acc = 0.f;
+#pragma unroll
+    for (int m = 0; m < Scr<D>::NV; m++) {
+        uint4 v = __ldg(p + m * 8);
+        const __half2 *h2 = reinterpret_cast<const __half2 *>(&v);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            float2 f = __half22float2(h2[e]);
+            float d0 = __fsub_rn(f.x, q[m * 8 + 2 * e]);
+            float d1 = __fsub_rn(f.y, q[m * 8 + 2 * e + 1]);
+            acc = __fmaf_rn(d0, d0, acc);
+            acc = __fmaf_rn(d1, d1, acc);
+        }
+    }
+    acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
+    acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
+    acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
+    return acc;
+}
+
+// Exact distance: warp-cooperative for numpy-mappable dims, else per lane.
+template <int D>
+__device__ __forceinline__ double exact_dist(const float *__restrict__ refs, int r, const float *__restrict__ q,
+                                             int dim, int gl)
+{
+    if constexpr (D > 0) {
+        const float *row = refs + (int64_t)r * D;
+        const int base = Lay<D>::base(gl);
+        const float *pr = row + base;
+        const float *pq = q + base;
+        double acc = sqdiff(__ldg(pr), __ldg(pq));
+#pragma unroll
+        for (int i = 1; i < Lay<D>::PER; i++) acc = __dadd_rn(acc, sqdiff(__ldg(pr + 8 * i), __ldg(pq + 8 * i)));
+        acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
+        acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
+        acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
+        if (Lay<D>::G == 16) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 8));
+        return __dsqrt_rn(acc);
+    } else {
+        return dist_thread(refs + (int64_t)r * dim, q, dim);
+    }
+}
+
+// One exact distance that every lane needs (prev / anchors).
+template <int D>
+__device__ __forceinline__ double exact_dist_all(const float *refs, int r, const float *q, int dim, int lane)
+{
+    if constexpr (D > 0) return exact_dist<D>(refs, r, q, dim, lane % Lay<D>::G);
+    else {
+        double v = 0.0;
+        if (lane == 0) v = dist_thread(refs + (int64_t)r * dim, q, dim);
+        return __shfl_sync(FULL, v, 0);
+    }
+}
+
+template <class IdxT>
+__device__ __forceinline__ uint32_t idx_at(const void *sidx, int64_t off)
+{
+    return (uint32_t)__ldg(reinterpret_cast<const IdxT *>(sidx) + off);
+}
+
+// D > 0: compile-time dim; D == 0: runtime dim (generic, exact only).
+template <int D, class IdxT>
+__global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
 {
     extern __shared__ uint32_t smem[];
     constexpr bool FAST = D > 0;
-    constexpr int G = FAST ? Lay<(FAST ? D : 64)>::G : 1;
-    constexpr int NG = WARP / G;
-    constexpr int PER = FAST ? Lay<(FAST ? D : 64)>::PER : 1;
-    constexpr int DD = FAST ? D : 64;
+    constexpr bool SCREEN = Scr<D>::on;
+    constexpr int GX = FAST ? Lay<(FAST ? D : 64)>::G : 1;  // lanes per exact distance
+    constexpr int NGX = WARP / GX;
+    constexpr int SP = Scr<(SCREEN ? D : 64)>::PER;
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
-    uint32_t *bm = smem + wib * (P.nw + HIT_CAP);
+    uint32_t *ws = smem + wib * K2_SMEM_WORDS;
+    uint32_t *hist = ws + 2 * SCAP;
     const int64_t gwarp = (int64_t)blockIdx.x * wpb + wib;
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
-    WarpList list{bm + P.nw, P.overflow + gwarp * P.n};
-    const int gl = lane % G, grp = lane / G;
     const int64_t n = P.n;
     const int dim = FAST ? D : P.dim;
+    uint32_t *spill = P.overflow + gwarp * 2 * n;
 
-    for (int w = lane; w < P.nw; w += 32) bm[w] = 0u;
-    __syncwarp();
-
-    unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0;
+    unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
 
     for (int64_t g = gwarp; g < P.Q; g += nwarps) {
+        QList A{ws, spill}, B{ws + SCAP, spill + n};
         const float *q = P.units + g * dim;
-        float qv[PER];
-        if (FAST) {
-            const int base = Lay<DD>::base(gl);
-#pragma unroll
-            for (int i = 0; i < PER; i++) qv[i] = __ldg(q + base + 8 * i);
-        }
-        auto dist = [&](int r) -> double {
-            if constexpr (FAST) return group_dist<DD>(P.refs + (int64_t)r * D, qv, gl);
-            else return dist_thread(P.refs + (int64_t)r * dim, q, dim);
-        };
-
         const int p = P.prev[g];
         if (p < 0 || p >= n) {
             if (lane == 0) atomicExch(P.err, ERR_PREV_RANGE);
             continue;
         }
-        // search.py:114-117: first ring around the previous match
-        double d = dist(p);
+        // ---- first ring around the previous match (search.py:114-117)
+        const double d = exact_dist_all<D>(P.refs, p, q, dim, lane);
+        long long exact_cnt = 1;
         int64_t lo, hi;
         ring_window(P.sdist + (int64_t)p * n, n, __dsub_rn(d, __dmul_rn(P.alpha, d)),
                     __dadd_rn(d, __dmul_rn(P.alpha, d)), lane, lo, hi);
-        {
-            const int32_t *ir = P.sidx + (int64_t)p * n;
-            for (int64_t k = lo + lane; k < hi; k += 32) {
-                int j = __ldg(ir + k);
-                atomicOr(&bm[j >> 5], 1u << (j & 31));
-            }
-        }
-        __syncwarp();
         int cS = (int)(hi - lo);
         const int first = cS;
-        int rings = 1;
-        long long evals = 1;
-
-        // used anchors still inside S (search.py:120-122), lane-distributed
-        int nu = 0, u_val = -1;
-        if (bit_test(bm, p)) {
-            nu = 1;
-            if (lane == 0) u_val = p;
+        bool p_in = false;
+        for (int64_t k = lo + lane; k < hi; k += 32) {
+            const uint32_t j = idx_at<IdxT>(P.sidx, (int64_t)p * n + k);
+            A.put((int)(k - lo), j);
+            p_in |= (j == (uint32_t)p);
         }
-        bool have_rng = false;
-        Pcg64 rng;
-        while (cS >= P.L && rings < P.max_rings) {
-            int na = cS - nu;
-            if (na <= 0) break;
-            if (!have_rng) {
-                if (P.key_words) {
-                    const uint32_t *kw = P.key_words + P.key_off[g];
-                    int nk = (int)(P.key_off[g + 1] - P.key_off[g]);
-                    pcg_seed(rng, [&](int i) { return __ldg(kw + i); }, nk);
-                } else {
-                    const uint32_t x = (uint32_t)(g % P.gw), y = (uint32_t)(P.gy0 + g / P.gw);
-                    const int snw = P.seed_nw;
-                    const uint32_t s0 = P.seed_lo, s1 = P.seed_hi, tt = P.t;
-                    pcg_seed(rng, [&](int i) -> uint32_t {
-                        if (i < snw) return i == 0 ? s0 : s1;
-                        i -= snw;
-                        return i == 0 ? x : (i == 1 ? y : tt);
-                    }, snw + 3);
+        p_in = __any_sync(FULL, p_in);
+        __threadfence_block();
+        __syncwarp();
+        int rings = 1;
+        long long tests = 0;
+        if (cS >= P.L && P.max_rings > 1) {
+            warp_radix_sort(A, B, cS, P.passes, hist, lane);
+            // used anchors still inside S (search.py:120-122), lane-distributed;
+            // r_u = their positions in S
+            int nu = 0, u_val = -1, u_pos = 0;
+            if (p_in) {
+                nu = 1;
+                if (lane == 0) {
+                    u_val = p;
+                    u_pos = list_lower_bound(A, cS, (uint32_t)p);
                 }
-                have_rng = true;
             }
-            // search.py:129: anchor = avail[integers(|avail|)], avail ascending
-            const int k = (int)pcg_integers(rng, (uint64_t)na);
-            if (lane < nu) atomicAnd(&bm[u_val >> 5], ~(1u << (u_val & 31)));
-            __syncwarp();
-            const int a = rank_select(bm, P.nw, k, lane);
-            __syncwarp();
-            if (lane < nu) atomicOr(&bm[u_val >> 5], 1u << (u_val & 31));
-            __syncwarp();
-            if (nu >= 32) {
-                if (lane == 0) atomicExch(P.err, ERR_USED_OVERFLOW);
-                break;
-            }
-            if (lane == nu) u_val = a;
-            nu++;
-            // search.py:131-135: ring around the anchor, intersect
-            const double da = dist(a);
-            evals++;
-            ring_window(P.sdist + (int64_t)a * n, n, __dsub_rn(da, __dmul_rn(P.alpha, da)),
-                        __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
-            const int32_t *ir = P.sidx + (int64_t)a * n;
-            int nh = 0;
-            for (int64_t kb = lo; kb < hi; kb += 128) {
-                int j0 = -1, j1 = -1, j2 = -1, j3 = -1;
-                int64_t k0 = kb + lane;
-                if (k0 < hi) j0 = __ldg(ir + k0);
-                if (k0 + 32 < hi) j1 = __ldg(ir + k0 + 32);
-                if (k0 + 64 < hi) j2 = __ldg(ir + k0 + 64);
-                if (k0 + 96 < hi) j3 = __ldg(ir + k0 + 96);
-                int js[4] = {j0, j1, j2, j3};
+            bool have_rng = false;
+            Pcg64 rng;
+            while (cS >= P.L && rings < P.max_rings) {
+                const int na = cS - nu;
+                if (na <= 0) break;
+                if (!have_rng) {
+                    if (P.key_words) {
+                        const uint32_t *kw = P.key_words + P.key_off[g];
+                        const int nk = (int)(P.key_off[g + 1] - P.key_off[g]);
+                        struct KW {
+                            const uint32_t *w;
+                            __device__ uint32_t operator()(int i) const { return __ldg(w + i); }
+                        } kf{kw};
+                        pcg_seed(rng, kf, nk);
+                    } else {
+                        struct FW {
+                            uint32_t s0, s1, x, y, t;
+                            int snw;
+                            __device__ uint32_t operator()(int i) const
+                            {
+                                if (i < snw) return i == 0 ? s0 : s1;
+                                i -= snw;
+                                return i == 0 ? x : (i == 1 ? y : t);
+                            }
+                        } fw{P.seed_lo, P.seed_hi, (uint32_t)(g % P.gw), (uint32_t)(P.gy0 + g / P.gw), P.t,
+                             P.seed_nw};
+                        pcg_seed(rng, fw, P.seed_nw + 3);
+                    }
+                    have_rng = true;
+                }
+                // search.py:129: anchor = avail[integers(|avail|)], avail = S \ used, ascending
+                const int k = (int)pcg_integers(rng, (uint64_t)na);
+                int pos = k;
+                for (int it = 0; it <= nu; it++) {
+                    const int c = __popc(__ballot_sync(FULL, lane < nu && u_pos <= pos));
+                    if (k + c == pos) break;
+                    pos = k + c;
+                }
+                const int a = (int)A.get(pos);
+                if (nu >= 32) {
+                    if (lane == 0) atomicExch(P.err, ERR_USED_OVERFLOW);
+                    break;
+                }
+                if (lane == nu) {
+                    u_val = a;
+                    u_pos = pos;
+                }
+                nu++;
+                // search.py:131-135: ring around the anchor, intersect with S
+                const double da = exact_dist_all<D>(P.refs, a, q, dim, lane);
+                exact_cnt++;
+                const double lv = __dsub_rn(da, __dmul_rn(P.alpha, da));
+                const double hv = __dadd_rn(da, __dmul_rn(P.alpha, da));
+                const float *drow = P.dmat + (int64_t)a * n;
+                int nh = 0;
+                for (int base = 0; base < cS; base += 128) {
+                    uint32_t j[4];
+                    float v[4];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int j = js[u];
-                    const bool hit = j >= 0 && bit_test(bm, j);
-                    const unsigned ball = __ballot_sync(FULL, hit);
-                    if (hit) list.put(nh + __popc(ball & lanemask_lt()), j);
-                    nh += __popc(ball);
+                    for (int u = 0; u < 4; u++) {
+                        const int i = base + u * 32 + lane;
+                        j[u] = i < cS ? A.get(i) : 0xffffffffu;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) v[u] = j[u] != 0xffffffffu ? __ldg(drow + j[u]) : 0.f;
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const double dv = (double)v[u];
+                        const bool keep = j[u] != 0xffffffffu && lv <= dv && dv <= hv;
+                        const unsigned ball = __ballot_sync(FULL, keep);
+                        if (keep) B.put(nh + __popc(ball & lanemask_lt()), j[u]);
+                        nh += __popc(ball);
+                    }
+                }
+                tests += cS;
+                rings++;
+                if (nh == 0) break;  // search.py:136-137 rollback: keep S
+                __threadfence_block();
+                __syncwarp();
+                {
+                    QList t = A;
+                    A = B;
+                    B = t;
+                }
+                cS = nh;
+                // used anchors still in S, with their new positions
+                bool keep = false;
+                if (lane < nu) {
+                    const double dv = (double)__ldg(drow + u_val);
+                    keep = lv <= dv && dv <= hv;
+                }
+                const unsigned kb = __ballot_sync(FULL, keep);
+                int nv = -1, np = 0;
+                int src = 0;
+                for (int i = 0; i < nu; i++) {
+                    const int vi = __shfl_sync(FULL, u_val, i);
+                    if ((kb >> i) & 1u) {
+                        if (lane == src) {
+                            nv = vi;
+                            np = list_lower_bound(A, cS, (uint32_t)vi);
+                        }
+                        src++;
+                    }
+                }
+                nu = src;
+                u_val = nv;
+                u_pos = np;
+                p_in = __any_sync(FULL, lane < nu && u_val == p);
+            }
+        } else if (cS > 0 && (cS < P.L || P.max_rings <= 1)) {
+            // no rings drawn: S is the unsorted window; order does not matter for
+            // the argmin, but the scanned output (batch API) must be ascending
+            if (P.scanned) warp_radix_sort(A, B, cS, P.passes, hist, lane);
+        }
+
+        // ---- final scan of S u {prev}, first minimum (search.py:140-143)
+        double bd = d;
+        int bi = p;
+        if constexpr (SCREEN) {
+            float qs[SP];
+            {
+                const int l8 = lane & 7;
+#pragma unroll
+                for (int m = 0; m < Scr<D>::NV; m++)
+#pragma unroll
+                    for (int e = 0; e < 8; e++) qs[m * 8 + e] = __ldg(q + m * 64 + l8 * 8 + e);
+            }
+            // pass 1: screened squared distances (stored as float bits in B)
+            const int grp8 = lane >> 3, l8 = lane & 7;
+            float ub_min = __double2float_ru(d);  // prev's exact distance bounds the minimum
+            for (int e0 = 0; e0 < cS; e0 += 4) {
+                const int e = e0 + grp8;
+                const bool valid = e < cS;
+                const uint32_t j = A.get(valid ? e : 0);
+                const float s = approx_sq<D>(P.refs16 + (int64_t)j * D, qs, l8);
+                // s relative error <= 32u (fp32, 27 rounded ops per path); fp16
+                // representation error of the reference row <= err16[j]
+                const float e16 = __ldg(P.err16 + j);
+                const float ub = __fadd_ru(__fsqrt_ru(__fmul_ru(s, 1.00001f)), __fadd_ru(e16, 1e-12f));
+                if (valid) {
+                    if (l8 == 0) B.put(e, __float_as_uint(s));
+                    ub_min = fminf(ub_min, ub);
                 }
             }
-            rings++;
-            if (nh == 0) break;  // search.py:136-137 rollback: keep S
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) ub_min = fminf(ub_min, __shfl_xor_sync(FULL, ub_min, o));
             __threadfence_block();
             __syncwarp();
-            for (int w = lane; w < P.nw; w += 32) bm[w] = 0u;
-            __syncwarp();
-            for (int e = lane; e < nh; e += 32) {
-                int j = list.get(e);
-                atomicOr(&bm[j >> 5], 1u << (j & 31));
-            }
-            __syncwarp();
-            cS = nh;
-            // keep only used anchors still in S
-            bool keep = lane < nu && bit_test(bm, u_val);
-            int nnu = 0, nv = -1;
-            for (int i = 0; i < nu; i++) {
-                int ki = __shfl_sync(FULL, (int)keep, i);
-                int vi = __shfl_sync(FULL, u_val, i);
-                if (ki) {
-                    if (lane == nnu) nv = vi;
-                    nnu++;
+            // pass 2: candidates whose lower bound reaches the best upper bound
+            int nsurv = 0;
+            for (int base = 0; base < cS; base += 32) {
+                const int e = base + lane;
+                bool surv = false;
+                uint32_t j = 0;
+                if (e < cS) {
+                    j = A.get(e);
+                    const float s = __uint_as_float(B.get(e));
+                    const float e16 = __ldg(P.err16 + j);
+                    const float lb = __fsub_rd(__fsqrt_rd(__fmul_rd(s, 0.99999f)), __fadd_ru(e16, 1e-12f));
+                    surv = lb <= ub_min;
+                }
+                const unsigned ball = __ballot_sync(FULL, surv);
+                if (surv) hist[(nsurv + __popc(ball & lanemask_lt())) & 255] = j;
+                const int add = __popc(ball);
+                // exact re-check in batches of up to 256 survivors
+                if (nsurv + add >= 224 || base + 32 >= cS) {
+                    __syncwarp();
+                    const int tot = nsurv + add;
+                    for (int s0 = 0; s0 < tot; s0 += NGX) {
+                        const int sidx2 = s0 + lane / GX;
+                        const bool ok = sidx2 < tot;
+                        const int jj = (int)hist[ok ? sidx2 : 0];
+                        const double dj = exact_dist<D>(P.refs, jj, q, dim, lane % GX);
+                        if (ok) argmin_merge(bd, bi, dj, jj);
+                    }
+                    exact_cnt += tot;
+                    nsurv = 0;
+                    __syncwarp();
+                } else {
+                    nsurv += add;
                 }
             }
-            nu = nnu;
-            u_val = nv;
-        }
-
-        // search.py:140-143: scan S u {prev}, first minimum (lowest index)
-        const bool p_in = bit_test(bm, p);
-        __syncwarp();
-        if (lane == 0 && !p_in) atomicOr(&bm[p >> 5], 1u << (p & 31));
-        __syncwarp();
-        const int nscan = cS + (p_in ? 0 : 1);
-        double bd = __longlong_as_double(0x7ff0000000000000LL);
-        int bi = 0x7fffffff;
-        int written = 0;
-        int32_t *sc_out = P.scanned ? P.scanned + g * (n + 1) : nullptr;
-        for (int wb = 0; wb < P.nw; wb += 32) {
-            uint32_t w = bm[wb + lane];
-            if (!__any_sync(FULL, w != 0u)) continue;
-            bm[wb + lane] = 0u;
-            const int pc = __popc(w);
-            const int inc = warp_incl_scan(pc, lane);
-            const int tot = __shfl_sync(FULL, inc, 31);
-            int pos = inc - pc;
-            while (w) {
-                int b = __ffs(w) - 1;
-                w &= w - 1;
-                int j = (wb + lane) * 32 + b;
-                list.sm[pos] = (uint32_t)j;
-                if (sc_out) sc_out[written + pos] = j;
-                pos++;
-            }
-            __syncwarp();
-            if constexpr (FAST) {
-                for (int e0 = 0; e0 < tot; e0 += NG) {
-                    const int e = e0 + grp;
-                    const bool valid = e < tot;
-                    const int j = (int)list.sm[valid ? e : 0];
-                    const double dj = dist(j);
+        } else {
+            for (int e0 = 0; e0 < cS; e0 += NGX) {
+                const int e = e0 + lane / GX;
+                const bool valid = e < cS;
+                const int j = (int)A.get(valid ? e : 0);
+                if constexpr (FAST) {
+                    const double dj = exact_dist<D>(P.refs, j, q, dim, lane % GX);
                     if (valid) argmin_merge(bd, bi, dj, j);
-                }
-            } else {
-                for (int e = lane; e < tot; e += 32) {
-                    const int j = (int)list.sm[e];
-                    argmin_merge(bd, bi, dist(j), j);
+                } else {
+                    if (valid) argmin_merge(bd, bi, dist_thread(P.refs + (int64_t)j * dim, q, dim), j);
                 }
             }
-            written += tot;
-            __syncwarp();
+            exact_cnt += cS;
         }
         warp_argmin(bd, bi);
-        evals += nscan;
+        const int nscan = cS + (p_in ? 0 : 1);
+        const long long evals = rings + nscan;
+        if (P.scanned) {
+            int32_t *so = P.scanned + g * (n + 1);
+            int below = 0;
+            for (int base = 0; base < cS; base += 32) {
+                const int e = base + lane;
+                uint32_t j = e < cS ? A.get(e) : 0xffffffffu;
+                below += __popc(__ballot_sync(FULL, e < cS && j < (uint32_t)p));
+                if (e < cS) so[e + ((!p_in && j > (uint32_t)p) ? 1 : 0)] = (int32_t)j;
+            }
+            if (!p_in && lane == 0) so[below] = p;
+        }
         if (lane == 0) {
             P.out_idx[g] = bi;
             P.out_dist[g] = bd;
@@ -514,12 +696,17 @@ __global__ void __launch_bounds__(256) query_kernel(QueryParams P)
         acc_e += evals;
         acc_c += cS;
         acc_f += first;
+        acc_t += tests;
+        acc_x += exact_cnt;
+        __syncwarp();
     }
     if (lane == 0 && P.stats) {
         atomicAdd(P.stats + 0, acc_r);
         atomicAdd(P.stats + 1, acc_e);
         atomicAdd(P.stats + 2, acc_c);
         atomicAdd(P.stats + 3, acc_f);
+        atomicAdd(P.stats + 4, acc_t);
+        atomicAdd(P.stats + 5, acc_x);
     }
 }
 
@@ -532,6 +719,46 @@ __global__ void ring_window_kernel(const float *row, int64_t n, double lv, doubl
         out[0] = lo;
         out[1] = hi;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Model preparation: fp16 screening copy of the references with a rigorous
+// per-row bound err16[j] >= ||r_j - fp16(r_j)|| (rounded up).
+__global__ void refs16_kernel(const float *refs, int64_t n, int dim, __half *r16, float *err)
+{
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double acc = 0.0;
+    for (int e = 0; e < dim; e++) {
+        float v = refs[j * dim + e];
+        __half h = __float2half_rn(v);
+        r16[j * dim + e] = h;
+        double dlt = (double)v - (double)__half2float(h);  // exact (both f32-representable, close)
+        acc = __fma_ru(dlt, dlt, acc);
+    }
+    err[j] = __double2float_ru(__dsqrt_ru(acc) * (1.0 + 1e-12));
+}
+
+// dmat[a][sidx[a][k]] = sdist[a][k]: index-ordered copy of the sorted rows.
+template <class IdxT>
+__global__ void dmat_scatter_kernel(const float *sdist, const IdxT *sidx, int64_t n, int64_t rows, float *dmat)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * n) return;
+    int64_t a = i / n;
+    dmat[a * n + (int64_t)sidx[i]] = sdist[i];
+}
+
+__global__ void narrow_u16_kernel(const int32_t *src, uint16_t *dst, int64_t cnt)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cnt) dst[i] = (uint16_t)src[i];
+}
+
+__global__ void widen_u16_kernel(const uint16_t *src, int32_t *dst, int64_t cnt)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cnt) dst[i] = (int32_t)src[i];
 }
 
 // ---------------------------------------------------------------------------

@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <type_traits>
 #include <array>
 #include <cstring>
 #include <string>
@@ -219,10 +220,11 @@ namespace {
 template <int D, class IdxT>
 int launch_query_t(riann_ctx *c, rb::QueryParams &P)
 {
-    const size_t per_warp = (size_t)rb::K2_SMEM_WORDS * 4;
+    const size_t per_warp = (size_t)rb::K2_SMEM_BYTES;
     const int wpb = 8;
     const size_t smem = per_warp * wpb;
-    auto kern = rb::query_kernel<D, IdxT>;
+    using LT = typename std::conditional<sizeof(IdxT) == 2, uint16_t, uint32_t>::type;
+    auto kern = rb::query_kernel<D, IdxT, LT>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
@@ -231,7 +233,7 @@ int launch_query_t(riann_ctx *c, rb::QueryParams &P)
     int64_t need = (P.Q + wpb - 1) / wpb;
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    RET(c->overflow.ensure((size_t)blocks * wpb * 2 * (size_t)c->n * 4));
+    RET(c->overflow.ensure((size_t)blocks * wpb * 2 * (size_t)c->n * (c->idx16 ? 2 : 4)));
     P.overflow = c->overflow.as<uint32_t>();
     kern<<<(unsigned)blocks, wpb * 32, smem, c->stream>>>(P);
     CK(cudaGetLastError());

@@ -226,19 +226,59 @@ struct QueryParams {
 };
 
 enum { ERR_PREV_RANGE = 3, ERR_USED_OVERFLOW = 5 };
-constexpr int SCAP = 1024;  // per-warp shared list capacity (entries); beyond it lists spill to global
-constexpr int K2_SMEM_WORDS = 2 * SCAP + 256;
+constexpr int LIST_BYTES = 4096;                      // per list, per warp, in shared memory
+constexpr int K2_SMEM_BYTES = 2 * LIST_BYTES + 1024;  // two lists + 256-word scratch
 
+// Candidate list: the first LIST_BYTES/sizeof(T) entries in shared memory,
+// the rest spilled to a per-warp global region.
+template <class T>
 struct QList {
-    uint32_t *sm;
-    uint32_t *gl;
-    __device__ __forceinline__ uint32_t get(int i) const { return i < SCAP ? sm[i] : gl[i - SCAP]; }
+    static constexpr int CAP = LIST_BYTES / (int)sizeof(T);
+    T *sm;
+    T *gl;
+    __device__ __forceinline__ uint32_t get(int i) const { return i < CAP ? (uint32_t)sm[i] : (uint32_t)gl[i - CAP]; }
     __device__ __forceinline__ void put(int i, uint32_t v) const
     {
-        if (i < SCAP) sm[i] = v;
-        else gl[i - SCAP] = v;
+        if (i < CAP) sm[i] = (T)v;
+        else gl[i - CAP] = (T)v;
     }
 };
+
+// L2 eviction-priority policies (createpolicy): the sorted tables and the
+// index-ordered distance matrix are streamed (evict_first, no L1 allocate);
+// the reference rows (f32 48 MB, fp16 24 MB at n=65,536) should stay L2-resident.
+__device__ __forceinline__ uint64_t pol_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float ld_stream(const float *a, uint64_t pol)
+{
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_keep16(const uint4 *a, uint64_t pol)
+{
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_keep(const float *a, uint64_t pol)
+{
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
 
 // search.py:77-79: lo = first v >= d-eps, hi = first v > d+eps (f32 values
 // compared as f64).  Lanes 0-15 search lo, lanes 16-31 search hi, 17-ary.
@@ -282,7 +322,8 @@ __device__ __forceinline__ void ring_window(const float *__restrict__ row, int64
 
 // Stable LSD radix sort (8-bit digits) of list a[0..cnt) using b as buffer;
 // the sorted result ends in `a` (the lists are swapped per pass).
-__device__ __forceinline__ void warp_radix_sort(QList &a, QList &b, int cnt, int passes, uint32_t *hist, int lane)
+template <class T>
+__device__ __forceinline__ void warp_radix_sort(QList<T> &a, QList<T> &b, int cnt, int passes, uint32_t *hist, int lane)
 {
     for (int ps = 0; ps < passes; ps++) {
         const int sh = 8 * ps;
@@ -316,7 +357,7 @@ __device__ __forceinline__ void warp_radix_sort(QList &a, QList &b, int cnt, int
             if (valid && rank == 0) hist[dg] = bse + (uint32_t)__popc(m);
             __syncwarp();
         }
-        QList t = a;
+        QList<T> t = a;
         a = b;
         b = t;
         __threadfence_block();
@@ -325,7 +366,8 @@ __device__ __forceinline__ void warp_radix_sort(QList &a, QList &b, int cnt, int
 }
 
 // first position in ascending list a[0..cnt) with value >= x (one lane)
-__device__ __forceinline__ int list_lower_bound(const QList &a, int cnt, uint32_t x)
+template <class T>
+__device__ __forceinline__ int list_lower_bound(const QList<T> &a, int cnt, uint32_t x)
 {
     int lo = 0, hi = cnt;
     while (lo < hi) {
@@ -346,13 +388,14 @@ struct Scr {
 };
 
 template <int D>
-__device__ __forceinline__ float approx_sq(const __half *__restrict__ row16, const float (&q)[Scr<D>::PER], int l8)
+__device__ __forceinline__ float approx_sq(const __half *__restrict__ row16, const float (&q)[Scr<D>::PER], int l8,
+                                           uint64_t pol)
 {
     const uint4 *p = reinterpret_cast<const uint4 *>(row16) + l8;
     float acc = 0.f;
 #pragma unroll
     for (int m = 0; m < Scr<D>::NV; m++) {
-        uint4 v = __ldg(p + m * 8);
+        uint4 v = ld_keep16(p + m * 8, pol);
         const __half2 *h2 = reinterpret_cast<const __half2 *>(&v);
 #pragma unroll
         for (int e = 0; e < 4; e++) {
@@ -411,31 +454,36 @@ __device__ __forceinline__ uint32_t idx_at(const void *sidx, int64_t off)
 }
 
 // D > 0: compile-time dim; D == 0: runtime dim (generic, exact only).
-template <int D, class IdxT>
+// IdxT: sorted index table element; LT: candidate-list element (u16 if n <= 65536).
+template <int D, class IdxT, class LT>
 __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
 {
-    extern __shared__ uint32_t smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool FAST = D > 0;
     constexpr bool SCREEN = Scr<D>::on;
     constexpr int GX = FAST ? Lay<(FAST ? D : 64)>::G : 1;  // lanes per exact distance
     constexpr int NGX = WARP / GX;
     constexpr int SP = Scr<(SCREEN ? D : 64)>::PER;
+    constexpr int SURV_CAP = 128;  // survivor slots (index + lower bound) in the scratch area
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
-    uint32_t *ws = smem + wib * K2_SMEM_WORDS;
-    uint32_t *hist = ws + 2 * SCAP;
+    unsigned char *ws = smem_raw + (size_t)wib * K2_SMEM_BYTES;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(ws + 2 * LIST_BYTES);
     const int64_t gwarp = (int64_t)blockIdx.x * wpb + wib;
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const int64_t n = P.n;
     const int dim = FAST ? D : P.dim;
-    uint32_t *spill = P.overflow + gwarp * 2 * n;
+    LT *spill = reinterpret_cast<LT *>(P.overflow) + gwarp * 2 * n;
+    const uint64_t pol_stream = pol_evict_first();
+    const uint64_t pol_keep = pol_evict_last();
 
     unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
 
     for (int64_t g = gwarp; g < P.Q; g += nwarps) {
-        QList A{ws, spill}, B{ws + SCAP, spill + n};
+        QList<LT> A{reinterpret_cast<LT *>(ws), spill};
+        QList<LT> B{reinterpret_cast<LT *>(ws + LIST_BYTES), spill + n};
         const float *q = P.units + g * dim;
         const int p = P.prev[g];
         if (p < 0 || p >= n) {
@@ -463,8 +511,8 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
         long long tests = 0;
         if (cS >= P.L && P.max_rings > 1) {
             warp_radix_sort(A, B, cS, P.passes, hist, lane);
-            // used anchors still inside S (search.py:120-122), lane-distributed;
-            // r_u = their positions in S
+            // used anchors still inside S (search.py:120-122), lane-distributed,
+            // with their positions in S
             int nu = 0, u_val = -1, u_pos = 0;
             if (p_in) {
                 nu = 1;
@@ -521,25 +569,26 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                     u_pos = pos;
                 }
                 nu++;
-                // search.py:131-135: ring around the anchor, intersect with S
+                // search.py:131-135: ring around the anchor, intersect with S by
+                // lookups in the anchor's index-ordered distance row
                 const double da = exact_dist_all<D>(P.refs, a, q, dim, lane);
                 exact_cnt++;
                 const double lv = __dsub_rn(da, __dmul_rn(P.alpha, da));
                 const double hv = __dadd_rn(da, __dmul_rn(P.alpha, da));
                 const float *drow = P.dmat + (int64_t)a * n;
                 int nh = 0;
-                for (int base = 0; base < cS; base += 128) {
-                    uint32_t j[4];
-                    float v[4];
+                for (int base = 0; base < cS; base += 256) {
+                    uint32_t j[8];
+                    float v[8];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < 8; u++) {
                         const int i = base + u * 32 + lane;
                         j[u] = i < cS ? A.get(i) : 0xffffffffu;
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; u++) v[u] = j[u] != 0xffffffffu ? __ldg(drow + j[u]) : 0.f;
+                    for (int u = 0; u < 8; u++) v[u] = j[u] != 0xffffffffu ? ld_stream(drow + j[u], pol_stream) : 0.f;
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < 8; u++) {
                         const double dv = (double)v[u];
                         const bool keep = j[u] != 0xffffffffu && lv <= dv && dv <= hv;
                         const unsigned ball = __ballot_sync(FULL, keep);
@@ -553,7 +602,7 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                 __threadfence_block();
                 __syncwarp();
                 {
-                    QList t = A;
+                    QList<LT> t = A;
                     A = B;
                     B = t;
                 }
@@ -561,7 +610,7 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                 // used anchors still in S, with their new positions
                 bool keep = false;
                 if (lane < nu) {
-                    const double dv = (double)__ldg(drow + u_val);
+                    const double dv = (double)ld_stream(drow + u_val, pol_stream);
                     keep = lv <= dv && dv <= hv;
                 }
                 const unsigned kb = __ballot_sync(FULL, keep);
@@ -582,79 +631,81 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                 u_pos = np;
                 p_in = __any_sync(FULL, lane < nu && u_val == p);
             }
-        } else if (cS > 0 && (cS < P.L || P.max_rings <= 1)) {
-            // no rings drawn: S is the unsorted window; order does not matter for
-            // the argmin, but the scanned output (batch API) must be ascending
-            if (P.scanned) warp_radix_sort(A, B, cS, P.passes, hist, lane);
+        } else if (cS > 0 && P.scanned) {
+            // no rings drawn: order is irrelevant to the argmin, but the scanned
+            // output (batch API) is ascending
+            warp_radix_sort(A, B, cS, P.passes, hist, lane);
         }
 
         // ---- final scan of S u {prev}, first minimum (search.py:140-143)
         double bd = d;
         int bi = p;
         if constexpr (SCREEN) {
+            // fp16 screening with a running upper bound; candidates whose lower
+            // bound can still reach the minimum go to the survivor slots and get
+            // the exact FP64 distance.
             float qs[SP];
-            {
-                const int l8 = lane & 7;
-#pragma unroll
-                for (int m = 0; m < Scr<D>::NV; m++)
-#pragma unroll
-                    for (int e = 0; e < 8; e++) qs[m * 8 + e] = __ldg(q + m * 64 + l8 * 8 + e);
-            }
-            // pass 1: screened squared distances (stored as float bits in B)
             const int grp8 = lane >> 3, l8 = lane & 7;
-            float ub_min = __double2float_ru(d);  // prev's exact distance bounds the minimum
+#pragma unroll
+            for (int m = 0; m < Scr<D>::NV; m++)
+#pragma unroll
+                for (int e = 0; e < 8; e++) qs[m * 8 + e] = __ldg(q + m * 64 + l8 * 8 + e);
+            uint32_t *sv_j = hist;                                       // survivor index
+            float *sv_lb = reinterpret_cast<float *>(hist + SURV_CAP);   // survivor lower bound
+            float ub_min = __double2float_ru(d);  // the previous match's exact distance
+            int nsv = 0;
+            auto flush = [&](bool all) {
+                // exact re-check of the survivors that can still win
+                __syncwarp();
+                int m = 0;
+                for (int b0 = 0; b0 < nsv; b0 += 32) {
+                    const int i = b0 + lane;
+                    const bool ok = i < nsv && sv_lb[i] <= ub_min;
+                    const uint32_t jj = i < nsv ? sv_j[i] : 0u;
+                    const unsigned ball = __ballot_sync(FULL, ok);
+                    __syncwarp();
+                    if (ok) sv_j[m + __popc(ball & lanemask_lt())] = jj;
+                    m += __popc(ball);
+                    __syncwarp();
+                }
+                for (int s0 = 0; s0 < m; s0 += NGX) {
+                    const int si = s0 + lane / GX;
+                    const bool ok = si < m;
+                    const int jj = (int)sv_j[ok ? si : 0];
+                    const double dj = exact_dist<D>(P.refs, jj, q, dim, lane % GX);
+                    if (ok) argmin_merge(bd, bi, dj, jj);
+                }
+                exact_cnt += m;
+                nsv = 0;
+                __syncwarp();
+                (void)all;
+            };
             for (int e0 = 0; e0 < cS; e0 += 4) {
                 const int e = e0 + grp8;
                 const bool valid = e < cS;
                 const uint32_t j = A.get(valid ? e : 0);
-                const float s = approx_sq<D>(P.refs16 + (int64_t)j * D, qs, l8);
-                // s relative error <= 32u (fp32, 27 rounded ops per path); fp16
-                // representation error of the reference row <= err16[j]
-                const float e16 = __ldg(P.err16 + j);
+                const float s = approx_sq<D>(P.refs16 + (int64_t)j * D, qs, l8, pol_keep);
+                // s: fp32 sum with relative error <= 29u; the fp16 row differs from
+                // the reference row by at most err16[j] in L2 norm
+                const float e16 = ld_keep(P.err16 + j, pol_keep);
                 const float ub = __fadd_ru(__fsqrt_ru(__fmul_ru(s, 1.00001f)), __fadd_ru(e16, 1e-12f));
-                if (valid) {
-                    if (l8 == 0) B.put(e, __float_as_uint(s));
-                    ub_min = fminf(ub_min, ub);
-                }
-            }
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) ub_min = fminf(ub_min, __shfl_xor_sync(FULL, ub_min, o));
-            __threadfence_block();
-            __syncwarp();
-            // pass 2: candidates whose lower bound reaches the best upper bound
-            int nsurv = 0;
-            for (int base = 0; base < cS; base += 32) {
-                const int e = base + lane;
-                bool surv = false;
-                uint32_t j = 0;
-                if (e < cS) {
-                    j = A.get(e);
-                    const float s = __uint_as_float(B.get(e));
-                    const float e16 = __ldg(P.err16 + j);
-                    const float lb = __fsub_rd(__fsqrt_rd(__fmul_rd(s, 0.99999f)), __fadd_ru(e16, 1e-12f));
-                    surv = lb <= ub_min;
-                }
+                const float lb = __fsub_rd(__fsqrt_rd(__fmul_rd(s, 0.99999f)), __fadd_ru(e16, 1e-12f));
+                float m = valid ? ub : ub_min;
+                m = fminf(m, __shfl_xor_sync(FULL, m, 8));
+                m = fminf(m, __shfl_xor_sync(FULL, m, 16));
+                ub_min = fminf(ub_min, m);
+                const bool surv = valid && l8 == 0 && lb <= ub_min;
                 const unsigned ball = __ballot_sync(FULL, surv);
-                if (surv) hist[(nsurv + __popc(ball & lanemask_lt())) & 255] = j;
                 const int add = __popc(ball);
-                // exact re-check in batches of up to 256 survivors
-                if (nsurv + add >= 224 || base + 32 >= cS) {
-                    __syncwarp();
-                    const int tot = nsurv + add;
-                    for (int s0 = 0; s0 < tot; s0 += NGX) {
-                        const int sidx2 = s0 + lane / GX;
-                        const bool ok = sidx2 < tot;
-                        const int jj = (int)hist[ok ? sidx2 : 0];
-                        const double dj = exact_dist<D>(P.refs, jj, q, dim, lane % GX);
-                        if (ok) argmin_merge(bd, bi, dj, jj);
-                    }
-                    exact_cnt += tot;
-                    nsurv = 0;
-                    __syncwarp();
-                } else {
-                    nsurv += add;
+                if (nsv + add > SURV_CAP) flush(false);
+                if (surv) {
+                    const int slot = nsv + __popc(ball & lanemask_lt());
+                    sv_j[slot] = j;
+                    sv_lb[slot] = lb;
                 }
+                nsv += add;
             }
+            flush(true);
         } else {
             for (int e0 = 0; e0 < cS; e0 += NGX) {
                 const int e = e0 + lane / GX;

@@ -73,6 +73,10 @@ void *riann_ctx_stream(riann_ctx *ctx);
 int riann_sync(riann_ctx *ctx);
 /* device bytes currently held by the context */
 uint64_t riann_ctx_device_bytes(riann_ctx *ctx);
+/* Frame-path selection: 0 = auto (anchor-grouped phases when n <= 65,536 and
+ * dim is 64 or 192, per-query kernel otherwise), 1 = per-query kernel only.
+ * Both produce identical results; the switch exists for testing. */
+int riann_ctx_set_path(riann_ctx *ctx, int path);
 
 /* ---- model (model.py:56-83 ReferenceModel) ----------------------------- */
 /* refs: (n, dim) float32 unit rows; patch (pw, ph); channels; metric_id must

@@ -48,6 +48,7 @@ SIGNATURES = {
     "riann_ctx_stream": (P, [P]),
     "riann_sync": (i32, [P]),
     "riann_ctx_device_bytes": (u64, [P]),
+    "riann_ctx_set_path": (i32, [P, i32]),
     "riann_model_set_refs": (i32, [P, P, i64, i32, i32, i32, i32, i32]),
     "riann_model_set_tables": (i32, [P, P, P]),
     "riann_model_build_tables": (i32, [P]),
@@ -201,3 +202,11 @@ def context(device: int | None = None) -> Context:
                 ctx = Context(d)
                 _contexts[d] = ctx
     return ctx
+
+
+def set_frame_path(path: int, device: int | None = None) -> None:
+    """0 = auto (anchor-grouped phases where supported), 1 = per-query kernel
+    only.  Results are identical; this exists for testing and measurement."""
+    ctx = context(device)
+    with ctx.lock:
+        check(lib().riann_ctx_set_path(ctx.h, int(path)))

@@ -7,6 +7,7 @@
 // GPU or returns an error.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <cstdarg>
@@ -19,7 +20,7 @@
 #include <vector>
 
 #include "riann_b200.h"
-#include "riann_kernels.cuh"
+#include "riann_bulk.cuh"
 
 namespace {
 
@@ -174,6 +175,11 @@ struct riann_ctx {
     bool tables = false;
     bool idx16 = false;  // sorted index table stored as uint16 (n <= 65536)
     DevBuf refs, refs16, err16, sdist, sidx, dmat;
+    DevBuf pos, coarse;  // rank rows and coarse index (bulk path, n <= 65536)
+    int ncoarse = 0;
+    bool bulk_disabled = false;
+    // bulk-path frame buffers
+    DevBuf b_state, b_pool, b_active[2], b_heavy, b_counters, b_counts, b_starts, b_grouped, b_scan_tmp;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -209,7 +215,8 @@ struct riann_ctx {
     }
     uint64_t bytes() const
     {
-        uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
+        uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + pos.cap + coarse.cap + b_state.cap +
+                     b_pool.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
                      fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap;
         return b;
     }
@@ -251,6 +258,125 @@ int launch_query_i(riann_ctx *c, rb::QueryParams &P)
     }
 }
 
+template <int D>
+int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
+{
+    const int64_t QN = Pq.Q, n = c->n;
+    RET(c->b_state.ensure((size_t)QN * sizeof(rb::QState)));
+    RET(c->b_pool.ensure((size_t)QN * rb::LIGHT_MAX * 2));
+    RET(c->b_active[0].ensure((size_t)QN * 4));
+    RET(c->b_active[1].ensure((size_t)QN * 4));
+    RET(c->b_heavy.ensure((size_t)QN * 4));
+    RET(c->b_grouped.ensure((size_t)QN * 4));
+    RET(c->b_counters.ensure(64));
+    RET(c->b_counts.ensure((size_t)(n + 1) * 4));
+    RET(c->b_starts.ensure((size_t)(n + 1) * 4));
+    size_t scan_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, c->b_counts.as<int32_t>(), c->b_starts.as<int32_t>(),
+                                     (int)(n + 1), c->stream));
+    RET(c->b_scan_tmp.ensure(scan_bytes));
+    int32_t *ctr = c->b_counters.as<int32_t>();  // [0..1] active counts, [2] heavy, [3] item counter
+    CK(cudaMemsetAsync(ctr, 0, 64, c->stream));
+
+    rb::BulkParams B;
+    memset(&B, 0, sizeof B);
+    B.refs = c->refs.as<float>();
+    B.refs16 = c->refs16.as<__half>();
+    B.err16 = c->err16.as<float>();
+    B.sdist = c->sdist.as<float>();
+    B.sidx = c->sidx.as<uint16_t>();
+    B.pos = c->pos.as<uint16_t>();
+    B.coarse = c->coarse.as<float>();
+    B.n = n;
+    B.ncoarse = c->ncoarse;
+    B.units = Pq.units;
+    B.prev = Pq.prev;
+    B.Q = QN;
+    B.seed_lo = Pq.seed_lo;
+    B.seed_hi = Pq.seed_hi;
+    B.seed_nw = Pq.seed_nw;
+    B.gw = Pq.gw;
+    B.gy0 = Pq.gy0;
+    B.t = Pq.t;
+    B.L = Pq.L;
+    B.alpha = Pq.alpha;
+    B.max_rings = Pq.max_rings;
+    B.passes = Pq.passes;
+    B.st = c->b_state.as<rb::QState>();
+    B.pool = c->b_pool.as<uint16_t>();
+    B.heavy = c->b_heavy.as<int32_t>();
+    B.n_heavy = ctr + 2;
+    B.counts = c->b_counts.as<int32_t>();
+    B.starts = c->b_starts.as<int32_t>();
+    B.grouped = c->b_grouped.as<int32_t>();
+    B.item_next = ctr + 3;
+    B.out_idx = Pq.out_idx;
+    B.out_dist = Pq.out_dist;
+    B.stats = Pq.stats;
+    B.err = Pq.err;
+
+    // P0
+    {
+        const int wpb = 8;
+        const size_t smem = (size_t)wpb * (2 * rb::LIGHT_MAX * 2 + 1024);
+        auto k = rb::bulk_p0_kernel<D>;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, wpb * 32, smem));
+        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::max(bps, 1), (QN + wpb - 1) / wpb);
+        B.active_out = c->b_active[0].as<int32_t>();
+        B.n_active_out = ctr + 0;
+        k<<<(unsigned)std::max<int64_t>(blocks, 1), wpb * 32, smem, c->stream>>>(B);
+        CK(cudaGetLastError());
+        c->launches += 1;
+    }
+    // ring phases
+    const size_t ring_smem = (((size_t)n * 2 + 15) & ~(size_t)15) + (size_t)((c->ncoarse + 3) & ~3) * 4 + D * 4;
+    auto rk = rb::bulk_ring_kernel<D>;
+    CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem));
+    const unsigned small_grid = (unsigned)c->sms * 4;
+    const int phases = Pq.max_rings - 1;
+    for (int ph = 0; ph < phases; ph++) {
+        const int in = ph & 1, out = in ^ 1;
+        B.active_in = c->b_active[in].as<int32_t>();
+        B.n_active_in = ctr + in;
+        B.active_out = c->b_active[out].as<int32_t>();
+        B.n_active_out = ctr + out;
+        if (ph >= 15) {  // long ring caps: stop once no query is left
+            int32_t h = 0;
+            CK(cudaMemcpyAsync(&h, ctr + in, 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            if (h == 0) break;
+        }
+        CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
+        CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
+        CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
+        rb::bulk_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
+        CK(cudaGetLastError());
+        CK(cub::DeviceScan::ExclusiveSum(c->b_scan_tmp.p, scan_bytes, B.counts, B.starts, (int)(n + 1), c->stream));
+        CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
+        rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
+        CK(cudaGetLastError());
+        rk<<<(unsigned)c->sms, rb::PH_WARPS * 32, ring_smem, c->stream>>>(B);
+        CK(cudaGetLastError());
+        c->launches += 3;
+    }
+    // final scan of the light queries
+    {
+        auto k = rb::bulk_final_kernel<D>;
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, 0));
+        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::max(bps, 1), (QN + 7) / 8);
+        k<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, c->stream>>>(B);
+        CK(cudaGetLastError());
+        c->launches += 1;
+    }
+    // heavy queries: the per-query kernel from scratch
+    Pq.qlist = B.heavy;
+    Pq.n_qlist = B.n_heavy;
+    return 1;
+}
+
 int launch_query(riann_ctx *c, rb::QueryParams &P)
 {
     P.refs16 = c->refs16.as<__half>();
@@ -259,6 +385,12 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     int bits = 1;
     while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
     P.passes = (bits + 7) / 8;
+    if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && !c->bulk_disabled &&
+        (c->dim == 64 || c->dim == 192)) {
+        int r = c->dim == 64 ? run_bulk_t<64>(c, P) : run_bulk_t<192>(c, P);
+        if (r != 1) return r;
+        // falls through: P.qlist = heavy queries
+    }
     return c->idx16 ? launch_query_i<uint16_t>(c, P) : launch_query_i<int32_t>(c, P);
 }
 
@@ -279,6 +411,30 @@ int check_err(riann_ctx *c)
     if (h == rb::ERR_USED_OVERFLOW)
         return fail(RIANN_E_UNSUPPORTED, "more than 32 used anchors remained in the candidate set");
     if (h) return fail(RIANN_E_CUDA, "kernel error %d", h);
+    return 0;
+}
+
+// rank rows + coarse index for the bulk path (needs the u16 index table)
+int build_bulk_tables(riann_ctx *c)
+{
+    if (!c->idx16) return 0;
+    const int64_t n = c->n;
+    c->ncoarse = (int)((n + rb::COARSE - 1) / rb::COARSE);
+    RET(c->pos.ensure((size_t)n * n * 2));
+    RET(c->coarse.ensure((size_t)n * c->ncoarse * 4));
+    const int64_t chunk = std::max<int64_t>(1, (int64_t)((1ull << 28) / (size_t)n));
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t rows = std::min<int64_t>(chunk, n - r0);
+        const int64_t m = rows * n;
+        rb::pos_scatter_kernel<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(
+            c->sidx.as<uint16_t>() + (size_t)r0 * n, n, rows, c->pos.as<uint16_t>() + (size_t)r0 * n);
+        CK(cudaGetLastError());
+    }
+    const int64_t mc = n * c->ncoarse;
+    rb::coarse_kernel<<<(unsigned)((mc + 255) / 256), 256, 0, c->stream>>>(c->sdist.as<float>(), n, c->ncoarse,
+                                                                          c->coarse.as<float>());
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
 
@@ -458,7 +614,9 @@ int riann_ctx_destroy(riann_ctx *c)
     if (!c) return 0;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
+    DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
+                      &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
+                      &c->b_grouped, &c->b_scan_tmp, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
                       &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,
@@ -485,6 +643,14 @@ int riann_sync(riann_ctx *c)
 
 uint64_t riann_ctx_device_bytes(riann_ctx *c) { return c ? c->bytes() : 0; }
 
+int riann_ctx_set_path(riann_ctx *c, int path)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (path < 0 || path > 1) return fail(RIANN_E_VALUE, "path must be 0 (auto) or 1 (per-query kernel)");
+    c->bulk_disabled = path == 1;
+    return 0;
+}
+
 int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, int pw, int ph, int channels,
                          int metric_id)
 {
@@ -500,6 +666,8 @@ int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, in
     c->sdist.release();
     c->sidx.release();
     c->dmat.release();
+    c->pos.release();
+    c->coarse.release();
     c->tables = false;
     RET(c->refs.ensure((size_t)n * dim * 4));
     CK(cudaMemcpyAsync(c->refs.p, refs, (size_t)n * dim * 4, cudaMemcpyHostToDevice, c->stream));
@@ -554,6 +722,7 @@ int riann_model_set_tables(riann_ctx *c, const float *sd, const int32_t *si)
         CK(cudaStreamSynchronize(c->stream));
     }
     stage.release();
+    RET(build_bulk_tables(c));
     c->tables = true;
     return 0;
 }
@@ -619,6 +788,7 @@ int riann_model_build_tables(riann_ctx *c)
     temp.release();
     d_off.release();
     c->keys.release();
+    RET(build_bulk_tables(c));
     c->tables = true;
     return 0;
 }

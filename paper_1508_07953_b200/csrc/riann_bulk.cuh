@@ -1,0 +1,577 @@
+// riann_bulk.cuh -- anchor-grouped ("bulk") frame path for models with n <= 65,536.
+//
+// The per-query kernel (K2) pays one random DRAM fetch (~64 B) per ring
+// membership test: ~4,000 tests per query at config 3.  Here the frame runs in
+// phases instead:
+//   P0   (warp per query): exact d_prev, first-ring window (coarse + fine
+//        search), window copy + radix sort into the query's candidate slot,
+//        first anchor draw (numpy RNG).
+//   ring phase k (<= max_rings-1 times): active queries are bucketed by their
+//        anchor (counting sort); one CTA loads an anchor's rank row
+//        pos[a][*] (u16, 128 KB) into shared memory once and filters the
+//        candidate lists of every query that drew that anchor (lo <= pos[a][j]
+//        < hi is exactly the searchsorted window test), then draws each
+//        query's next anchor.
+//   F    (warp per query): fp16-screened final scan of S u {prev} with exact
+//        FP64 re-check.
+// A query that does not fit (first ring > LIGHT_MAX, > BULK_U used anchors
+// still in S) is marked heavy and recomputed from scratch by K2, so results
+// never depend on the path taken.
+#pragma once
+
+#include "riann_kernels.cuh"
+
+namespace rb {
+
+constexpr int LIGHT_MAX = 2048;  // candidate slot size (u16 entries) = smem list capacity
+constexpr int BULK_U = 4;        // used anchors tracked per query
+constexpr int COARSE = 64;       // coarse index stride of the sorted rows
+constexpr int PH_WARPS = 16;     // warps per ring-phase CTA
+constexpr int PH_CHUNK = 64;     // queries per ring-phase work item
+
+enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
+
+struct __align__(16) QState {
+    double d_prev;
+    uint64_t sh, sl, ih, il;  // PCG64 state and increment
+    int32_t cS, first, rings, status;
+    int32_t anchor, nu, rng_has, p_in;
+    uint32_t rng_buf;
+    int32_t tests, exact, pad;
+    int32_t u[BULK_U];
+};
+
+struct BulkParams {
+    const float *refs;
+    const __half *refs16;
+    const float *err16;
+    const float *sdist;
+    const uint16_t *sidx;
+    const uint16_t *pos;     // rank rows: pos[a][sidx[a][k]] = k
+    const float *coarse;     // coarse[a][b] = sdist[a][b*COARSE]
+    int64_t n;
+    int ncoarse;
+    const float *units;
+    const int32_t *prev;
+    int64_t Q;
+    uint32_t seed_lo, seed_hi;
+    int seed_nw;
+    int gw, gy0;
+    uint32_t t;
+    int L;
+    double alpha;
+    int max_rings;
+    int passes;
+    QState *st;
+    uint16_t *pool;          // Q * LIGHT_MAX candidate slots
+    int32_t *active_in;      // queries whose anchor is pending (this phase)
+    const int32_t *n_active_in;
+    int32_t *active_out;     // next phase
+    int32_t *n_active_out;
+    int32_t *heavy;          // queries for K2
+    int32_t *n_heavy;
+    int32_t *counts;         // per anchor row (n + 1)
+    int32_t *starts;         // exclusive scan of counts
+    int32_t *grouped;        // active queries grouped by anchor
+    int32_t *item_next;      // work-item counter
+    int32_t *out_idx;
+    double *out_dist;
+    unsigned long long *stats;
+    int *err;
+};
+
+__device__ __forceinline__ void seed_frame(Pcg64 &rng, const BulkParams &P, int64_t g)
+{
+    struct FW {
+        uint32_t s0, s1, x, y, t;
+        int snw;
+        __device__ uint32_t operator()(int i) const
+        {
+            if (i < snw) return i == 0 ? s0 : s1;
+            i -= snw;
+            return i == 0 ? x : (i == 1 ? y : t);
+        }
+    } fw{P.seed_lo, P.seed_hi, (uint32_t)(g % P.gw), (uint32_t)(P.gy0 + g / P.gw), P.t, P.seed_nw};
+    pcg_seed(rng, fw, P.seed_nw + 3);
+}
+
+__device__ __forceinline__ void rng_load(Pcg64 &r, const QState &s)
+{
+    r.sh = s.sh;
+    r.sl = s.sl;
+    r.ih = s.ih;
+    r.il = s.il;
+    r.has = s.rng_has;
+    r.buf = s.rng_buf;
+}
+
+__device__ __forceinline__ void rng_store(QState &s, const Pcg64 &r)
+{
+    s.sh = r.sh;
+    s.sl = r.sl;
+    s.ih = r.ih;
+    s.il = r.il;
+    s.rng_has = r.has;
+    s.rng_buf = r.buf;
+}
+
+// searchsorted pair on a sorted row through its coarse index: returns
+// lo = first v >= lv and hi = first v > hv.  The coarse array (shared or global
+// memory) is searched 17-ary by the two half-warps (as ring_window); the
+// remaining <= 65 entries of the row are counted.
+__device__ __forceinline__ void window_coarse(const float *__restrict__ row, const float *cs, int nb, int64_t n,
+                                              double lv, double hv, int lane, int64_t &lo, int64_t &hi)
+{
+    const int h = lane >> 4, hl = lane & 15;
+    const double thr = h ? hv : lv;
+    int b0 = 0, b1 = nb;  // first coarse entry failing the predicate lies in [b0, b1]
+    for (;;) {
+        const int s = b1 - b0;
+        if (!__any_sync(FULL, s > 16)) break;
+        const int p = b0 + (int)(((int64_t)(hl + 1) * s) / 17);
+        bool pr = false;
+        if (s > 16) {
+            const double v = (double)cs[p];
+            pr = h ? (v <= thr) : (v < thr);
+        }
+        const unsigned ball = __ballot_sync(FULL, pr);
+        const int c = __popc((ball >> (h * 16)) & 0xffffu);
+        const int p_lo = __shfl_sync(FULL, p, h * 16 + (c > 0 ? c - 1 : 0));
+        const int p_hi = __shfl_sync(FULL, p, h * 16 + (c < 16 ? c : 15));
+        if (s > 16) {
+            if (c > 0) b0 = p_lo + 1;
+            if (c < 16) b1 = p_hi;
+        }
+    }
+    {
+        const int p = b0 + hl;
+        bool pr = false;
+        if (p < b1) {
+            const double v = (double)cs[p];
+            pr = h ? (v <= thr) : (v < thr);
+        }
+        const unsigned ball = __ballot_sync(FULL, pr);
+        b0 += __popc((ball >> (h * 16)) & 0xffffu);
+    }
+    const int b = b0;  // coarse entries [0, b) satisfy the predicate
+    const int64_t s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
+    const int64_t s1 = (b < nb) ? (int64_t)b * COARSE : n;
+    int cnt = 0;
+    for (int64_t k = s0 + hl; k < s1; k += 16) {
+        const double v = (double)__ldg(row + k);
+        cnt += (h ? (v <= thr) : (v < thr)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    const int64_t res = s0 + cnt;
+    lo = __shfl_sync(FULL, res, 0);
+    hi = __shfl_sync(FULL, res, 16);
+}
+
+// k-th (0-based) element of ascending list S minus the used anchors u[0..nu)
+// (search.py:122, 129).  upos: positions of the used anchors in S.
+__device__ __forceinline__ int avail_pos(int k, const int *upos, int nu)
+{
+    int pos = k;
+    for (int it = 0; it <= nu; it++) {
+        int c = 0;
+        for (int i = 0; i < nu; i++) c += upos[i] <= pos ? 1 : 0;
+        if (k + c == pos) break;
+        pos = k + c;
+    }
+    return pos;
+}
+
+__device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int cnt, uint32_t x)
+{
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((uint32_t)a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------
+// P0: first ring, candidate slot, first anchor.  One warp per query.
+template <int D>
+__global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    unsigned char *ws = smem_raw + (size_t)wib * (2 * LIGHT_MAX * 2 + 1024);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(ws + 4 * LIGHT_MAX);
+    const int64_t nwarps = (int64_t)gridDim.x * wpb;
+    const int64_t n = P.n;
+    for (int64_t g = (int64_t)blockIdx.x * wpb + wib; g < P.Q; g += nwarps) {
+        QList<uint16_t> A{reinterpret_cast<uint16_t *>(ws), nullptr};
+        QList<uint16_t> B{reinterpret_cast<uint16_t *>(ws + 2 * LIGHT_MAX), nullptr};
+        const float *q = P.units + g * D;
+        const int p = P.prev[g];
+        QState s;
+        s.status = ST_DONE;
+        if (p < 0 || p >= n) {
+            if (lane == 0) atomicExch(P.err, ERR_PREV_RANGE);
+            if (lane == 0) P.st[g].status = ST_HEAVY + 100;  // skipped everywhere
+            continue;
+        }
+        const double d = exact_dist_all<D>(P.refs, p, q, D, lane);
+        int64_t lo, hi;
+        window_coarse(P.sdist + (int64_t)p * n, P.coarse + (int64_t)p * P.ncoarse, P.ncoarse, n,
+                      __dsub_rn(d, __dmul_rn(P.alpha, d)), __dadd_rn(d, __dmul_rn(P.alpha, d)), lane, lo, hi);
+        const int cS = (int)(hi - lo);
+        if (cS > LIGHT_MAX) {
+            if (lane == 0) {
+                P.st[g].status = ST_HEAVY;
+                P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
+            }
+            continue;
+        }
+        bool p_in = false;
+        for (int64_t k = lo + lane; k < hi; k += 32) {
+            const uint32_t j = __ldg(P.sidx + (int64_t)p * n + k);
+            A.sm[k - lo] = (uint16_t)j;
+            p_in |= (j == (uint32_t)p);
+        }
+        p_in = __any_sync(FULL, p_in);
+        __syncwarp();
+        const bool loop = cS >= P.L && P.max_rings > 1;
+        if (loop) warp_radix_sort(A, B, cS, P.passes, hist, lane);
+        // candidate slot (16-byte aligned): g * LIGHT_MAX
+        uint16_t *slot = P.pool + g * LIGHT_MAX;
+        {
+            const uint4 *src = reinterpret_cast<const uint4 *>(A.sm);
+            uint4 *dst = reinterpret_cast<uint4 *>(slot);
+            for (int i = lane; i < (cS + 7) / 8; i += 32) dst[i] = src[i];
+        }
+        if (lane == 0) {
+            s.d_prev = d;
+            s.cS = cS;
+            s.first = cS;
+            s.rings = 1;
+            s.tests = 0;
+            s.exact = 1;
+            s.p_in = p_in;
+            s.nu = 0;
+            s.rng_has = 0;
+            s.rng_buf = 0;
+            s.sh = s.sl = s.ih = s.il = 0;
+            int upos[BULK_U];
+            if (p_in) {
+                s.u[0] = p;
+                upos[0] = lower_bound_u16(A.sm, cS, (uint32_t)p);
+                s.nu = 1;
+            }
+            if (loop && cS - s.nu > 0) {
+                Pcg64 rng;
+                seed_frame(rng, P, g);
+                const int k = (int)pcg_integers(rng, (uint64_t)(cS - s.nu));
+                const int pos = avail_pos(k, upos, s.nu);
+                s.anchor = (int)A.sm[pos];
+                s.u[s.nu++] = s.anchor;
+                rng_store(s, rng);
+                s.status = ST_ACTIVE;
+                P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+            } else {
+                s.status = ST_DONE;
+            }
+            P.st[g] = s;
+        }
+        __syncwarp();
+    }
+}
+
+// counting sort of the active queries by anchor row
+__global__ void bulk_count_kernel(BulkParams P)
+{
+    const int m = *P.n_active_in;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        atomicAdd(P.counts + P.st[P.active_in[i]].anchor, 1);
+}
+
+__global__ void bulk_scatter_kernel(BulkParams P)
+{
+    const int m = *P.n_active_in;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const int g = P.active_in[i];
+        const int a = P.st[g].anchor;
+        P.grouped[P.starts[a] + atomicAdd(P.counts + a, 1)] = g;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Ring phase: CTA per work item (PH_CHUNK consecutive grouped queries); the
+// anchor's rank row lives in shared memory while its queries are filtered.
+template <int D>
+__global__ void __launch_bounds__(PH_WARPS * 32, 1) bulk_ring_kernel(BulkParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint16_t *prow = reinterpret_cast<uint16_t *>(smem_raw);                       // n entries
+    float *crow = reinterpret_cast<float *>(smem_raw + ((P.n * 2 + 15) & ~15LL));  // ncoarse
+    float *rrow = crow + ((P.ncoarse + 3) & ~3);                                   // D floats
+    __shared__ int s_item, s_run_end;
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int64_t n = P.n;
+    const int m = *P.n_active_in;
+    const int nitems = (m + PH_CHUNK - 1) / PH_CHUNK;
+    const uint64_t pol_keep = pol_evict_last();
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(P.item_next, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= nitems) break;
+        const int e0 = item * PH_CHUNK, e1 = min(m, e0 + PH_CHUNK);
+        int run0 = e0;
+        while (run0 < e1) {
+            // run of equal anchors
+            const int a = P.st[P.grouped[run0]].anchor;
+            if (threadIdx.x == 0) {
+                int r = run0 + 1;
+                while (r < e1 && P.st[P.grouped[r]].anchor == a) r++;
+                s_run_end = r;
+            }
+            // load the anchor's rank row, coarse row and reference row
+            {
+                const uint4 *src = reinterpret_cast<const uint4 *>(P.pos + (int64_t)a * n);
+                uint4 *dst = reinterpret_cast<uint4 *>(prow);
+                const int nv = (int)(n / 8);
+                for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = __ldcs(src + i);
+                for (int i = nv * 8 + threadIdx.x; i < n; i += blockDim.x) prow[i] = P.pos[(int64_t)a * n + i];
+                for (int i = threadIdx.x; i < P.ncoarse; i += blockDim.x)
+                    crow[i] = P.coarse[(int64_t)a * P.ncoarse + i];
+                for (int i = threadIdx.x; i < D; i += blockDim.x) rrow[i] = P.refs[(int64_t)a * D + i];
+            }
+            __syncthreads();
+            const int run1 = s_run_end;
+            for (int e = run0 + w; e < run1; e += PH_WARPS) {
+                const int64_t g = P.grouped[e];
+                QState s = P.st[g];
+                const float *q = P.units + g * D;
+                // search.py:131-133: exact d_a (numpy order), window on row a
+                double da;
+                {
+                    const int gl = lane % Lay<D>::G;
+                    const int base = Lay<D>::base(gl);
+                    double acc = sqdiff(rrow[base], __ldg(q + base));
+#pragma unroll
+                    for (int i = 1; i < Lay<D>::PER; i++) acc = __dadd_rn(acc, sqdiff(rrow[base + 8 * i], __ldg(q + base + 8 * i)));
+                    acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
+                    acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
+                    acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
+                    if (Lay<D>::G == 16) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 8));
+                    da = __dsqrt_rn(acc);
+                }
+                int64_t lo, hi;
+                window_coarse(P.sdist + (int64_t)a * n, crow, P.ncoarse, n, __dsub_rn(da, __dmul_rn(P.alpha, da)),
+                              __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
+                // search.py:134: S' = S n ring, order kept, filtered in place
+                uint16_t *slot = P.pool + g * LIGHT_MAX;
+                const int cS = s.cS;
+                int nh = 0;
+                for (int base = 0; base < cS; base += 256) {
+                    const int i0 = base + lane * 8;
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (i0 < cS) v = *reinterpret_cast<const uint4 *>(slot + i0);
+                    const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
+                    unsigned keepm = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        if (i0 + k < cS) {
+                            const int pk = prow[e8[k]];
+                            if (pk >= lo && pk < hi) keepm |= 1u << k;
+                        }
+                    }
+                    const int kc = __popc(keepm);
+                    const int inc = warp_incl_scan(kc, lane);
+                    const int tot = __shfl_sync(FULL, inc, 31);
+                    __syncwarp();
+                    if (tot > 0) {
+                        int o = nh + inc - kc;
+#pragma unroll
+                        for (int k = 0; k < 8; k++)
+                            if ((keepm >> k) & 1u) slot[o++] = e8[k];
+                    }
+                    nh += tot;
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    s.tests += cS;
+                    s.exact += 1;
+                    s.rings += 1;
+                    if (nh == 0) {
+                        s.status = ST_DONE;  // search.py:136-137 rollback
+                    } else {
+                        s.cS = nh;
+                        // used anchors still in S
+                        int nu = 0;
+                        for (int i = 0; i < s.nu; i++) {
+                            const int pk = prow[s.u[i]];
+                            if (pk >= lo && pk < hi) s.u[nu++] = s.u[i];
+                        }
+                        s.nu = nu;
+                        bool pin = false;
+                        for (int i = 0; i < nu; i++) pin |= s.u[i] == P.prev[g];
+                        s.p_in = pin;
+                        s.status = ST_DONE;
+                        if (nh >= P.L && s.rings < P.max_rings && nh - nu > 0) {
+                            int upos[BULK_U];
+                            for (int i = 0; i < nu; i++) upos[i] = lower_bound_u16(slot, nh, (uint32_t)s.u[i]);
+                            Pcg64 rng;
+                            rng_load(rng, s);
+                            const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
+                            const int pos = avail_pos(k, upos, nu);
+                            if (nu >= BULK_U) {
+                                s.status = ST_HEAVY;
+                                P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
+                            } else {
+                                s.anchor = (int)slot[pos];
+                                s.u[s.nu++] = s.anchor;
+                                rng_store(s, rng);
+                                s.status = ST_ACTIVE;
+                                P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+                            }
+                        }
+                    }
+                    P.st[g] = s;
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            run0 = run1;
+        }
+    }
+    (void)pol_keep;
+}
+
+// ---------------------------------------------------------------------------
+// F: final scan of S u {prev} for every light query (status DONE).
+template <int D>
+__global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P)
+{
+    constexpr int GX = Lay<D>::G;
+    constexpr int NGX = WARP / GX;
+    constexpr int SP = Scr<D>::PER;
+    constexpr int SURV_CAP = 128;
+    __shared__ __align__(16) uint32_t sv_all[8][2 * SURV_CAP];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    uint32_t *sv_j = sv_all[wib];
+    float *sv_lb = reinterpret_cast<float *>(sv_all[wib] + SURV_CAP);
+    const int64_t nwarps = (int64_t)gridDim.x * wpb;
+    const uint64_t pol_keep = pol_evict_last();
+    unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
+    for (int64_t g = (int64_t)blockIdx.x * wpb + wib; g < P.Q; g += nwarps) {
+        const QState &sr = P.st[g];
+        const int status = sr.status;
+        if (status != ST_DONE) continue;
+        const int cS = sr.cS;
+        const int p = P.prev[g];
+        const double d = sr.d_prev;
+        const float *q = P.units + g * D;
+        const uint16_t *slot = P.pool + g * LIGHT_MAX;
+        double bd = d;
+        int bi = p;
+        long long exact_cnt = sr.exact;
+        float qs[SP];
+        const int grp8 = lane >> 3, l8 = lane & 7;
+#pragma unroll
+        for (int mm = 0; mm < Scr<D>::NV; mm++)
+#pragma unroll
+            for (int e = 0; e < 8; e++) qs[mm * 8 + e] = __ldg(q + mm * 64 + l8 * 8 + e);
+        float ub_min = __double2float_ru(d);
+        int nsv = 0;
+        auto flush = [&]() {
+            __syncwarp();
+            int mcount = 0;
+            for (int b0 = 0; b0 < nsv; b0 += 32) {
+                const int i = b0 + lane;
+                const bool ok = i < nsv && sv_lb[i] <= ub_min;
+                const uint32_t jj = i < nsv ? sv_j[i] : 0u;
+                const unsigned ball = __ballot_sync(FULL, ok);
+                __syncwarp();
+                if (ok) sv_j[mcount + __popc(ball & lanemask_lt())] = jj;
+                mcount += __popc(ball);
+                __syncwarp();
+            }
+            for (int s0 = 0; s0 < mcount; s0 += NGX) {
+                const int si = s0 + lane / GX;
+                const bool ok = si < mcount;
+                const int jj = (int)sv_j[ok ? si : 0];
+                const double dj = exact_dist<D>(P.refs, jj, q, D, lane % GX);
+                if (ok) argmin_merge(bd, bi, dj, jj);
+            }
+            exact_cnt += mcount;
+            nsv = 0;
+            __syncwarp();
+        };
+        for (int e0 = 0; e0 < cS; e0 += 4) {
+            const int e = e0 + grp8;
+            const bool valid = e < cS;
+            const uint32_t j = slot[valid ? e : 0];
+            const float s = approx_sq<D>(P.refs16 + (int64_t)j * D, qs, l8, pol_keep);
+            const float e16 = ld_keep(P.err16 + j, pol_keep);
+            const float ub = __fadd_ru(__fsqrt_ru(__fmul_ru(s, 1.00001f)), __fadd_ru(e16, 1e-12f));
+            const float lb = __fsub_rd(__fsqrt_rd(__fmul_rd(s, 0.99999f)), __fadd_ru(e16, 1e-12f));
+            float mv = valid ? ub : ub_min;
+            mv = fminf(mv, __shfl_xor_sync(FULL, mv, 8));
+            mv = fminf(mv, __shfl_xor_sync(FULL, mv, 16));
+            ub_min = fminf(ub_min, mv);
+            const bool surv = valid && l8 == 0 && lb <= ub_min;
+            const unsigned ball = __ballot_sync(FULL, surv);
+            const int add = __popc(ball);
+            if (nsv + add > SURV_CAP) flush();
+            if (surv) {
+                const int slot2 = nsv + __popc(ball & lanemask_lt());
+                sv_j[slot2] = j;
+                sv_lb[slot2] = lb;
+            }
+            nsv += add;
+        }
+        flush();
+        warp_argmin(bd, bi);
+        const int nscan = cS + (sr.p_in ? 0 : 1);
+        if (lane == 0) {
+            P.out_idx[g] = bi;
+            P.out_dist[g] = bd;
+        }
+        acc_r += sr.rings;
+        acc_e += sr.rings + nscan;
+        acc_c += cS;
+        acc_f += sr.first;
+        acc_t += sr.tests;
+        acc_x += exact_cnt;
+        __syncwarp();
+    }
+    if (lane == 0 && P.stats) {
+        atomicAdd(P.stats + 0, acc_r);
+        atomicAdd(P.stats + 1, acc_e);
+        atomicAdd(P.stats + 2, acc_c);
+        atomicAdd(P.stats + 3, acc_f);
+        atomicAdd(P.stats + 4, acc_t);
+        atomicAdd(P.stats + 5, acc_x);
+    }
+}
+
+// rank rows and coarse rows of the sorted tables (built once per model)
+__global__ void pos_scatter_kernel(const uint16_t *sidx, int64_t n, int64_t rows, uint16_t *pos)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * n) return;
+    int64_t a = i / n;
+    pos[a * n + sidx[i]] = (uint16_t)(i - a * n);
+}
+
+__global__ void coarse_kernel(const float *sdist, int64_t n, int nb, float *coarse)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * nb) return;
+    int64_t a = i / nb, b = i - a * nb;
+    coarse[i] = sdist[a * n + b * COARSE];
+}
+
+}  // namespace rb

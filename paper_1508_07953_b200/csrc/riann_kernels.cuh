@@ -223,6 +223,8 @@ struct QueryParams {
     int *err;
     uint32_t *overflow;   // per warp: 2n entries (list spill)
     int passes;           // radix passes for indices < n
+    const int32_t *qlist; // optional: process only these queries (count *n_qlist)
+    const int32_t *n_qlist;
 };
 
 enum { ERR_PREV_RANGE = 3, ERR_USED_OVERFLOW = 5 };
@@ -480,8 +482,10 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
     const uint64_t pol_keep = pol_evict_last();
 
     unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
+    const int64_t qn = P.qlist ? (int64_t)*P.n_qlist : P.Q;
 
-    for (int64_t g = gwarp; g < P.Q; g += nwarps) {
+    for (int64_t gi = gwarp; gi < qn; gi += nwarps) {
+        const int64_t g = P.qlist ? (int64_t)P.qlist[gi] : gi;
         QList<LT> A{reinterpret_cast<LT *>(ws), spill};
         QList<LT> B{reinterpret_cast<LT *>(ws + LIST_BYTES), spill + n};
         const float *q = P.units + g * dim;

@@ -291,3 +291,33 @@ def test_engine_properties(R):
     u2 = R.frame_units(moved, model)
     diff = u2.astype(np.float64) - unit.astype(np.float64)
     assert s2.temporal_change == float(np.sum(np.sqrt(np.sum(diff * diff, axis=1))))
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_frame_paths_identical(R, oracle_mod, path):
+    """The anchor-grouped (bulk) frame path and the per-query kernel give the
+    same bits as the oracle (D=64 config 0 and D=192 RGB clip)."""
+    from dataclasses import replace
+
+    from paper_1508_07953_b200 import _native as N
+    from paper_1508_07953_b200 import workloads as W
+
+    N.set_frame_path(path)
+    try:
+        for cfg in (W.CONFIGS[0], replace(W.CONFIGS[3], height=40, width=96, frames=3, n_refs=4096)):
+            frames = W.clip(cfg, 3)
+            refs = W.reference_set(cfg)
+            model = R.ReferenceModel.from_refs(refs, cfg.patch, channels=cfg.channels)
+            sd, si = model.table_rows(0, model.n)
+            om = oracle_mod.OracleModel(refs, sd, si)
+            gw, gh = cfg.grid
+            prev = oracle_mod.init_field_indices(gw, gh, model.n, 0)
+            for t, (_, fld, st) in enumerate(R.stream_fields(model, frames)):
+                idx, dist, ost, _ = oracle_mod.process_frame(om, frames[t], prev, cfg.patch, t + 1)
+                assert np.array_equal(fld.indices, idx), (cfg.name, t)
+                assert np.array_equal(_bits(fld.distances), _bits(dist)), (cfg.name, t)
+                assert st.total_distance_evals == ost["total_distance_evals"]
+                assert st.total_rings == ost["total_rings"]
+                prev = idx
+    finally:
+        N.set_frame_path(0)

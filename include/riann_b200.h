@@ -60,6 +60,7 @@ typedef struct {
     double temporal_change;
     uint64_t sum_ring_tests;   /* sum over rings of |S| membership lookups */
     uint64_t sum_exact_evals;  /* FP64 distances actually evaluated (screening survivors) */
+    uint64_t queries_fallback; /* queries the anchor-grouped path handed to the per-query kernel */
 } riann_frame_stats;
 
 int riann_abi_version(void);

@@ -33,6 +33,7 @@ class FrameStatsC(C.Structure):
         ("temporal_change", C.c_double),
         ("sum_ring_tests", C.c_uint64),
         ("sum_exact_evals", C.c_uint64),
+        ("queries_fallback", C.c_uint64),
     ]
 
 

@@ -331,7 +331,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         c->launches += 1;
     }
     // ring phases
-    const size_t ring_smem = (((size_t)n * 2 + 15) & ~(size_t)15) + (size_t)((c->ncoarse + 3) & ~3) * 4 + D * 4;
+    const size_t ring_smem = ((size_t)n * 2 + 127) & ~(size_t)127;
     auto rk = rb::bulk_ring_kernel<D>;
     CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem));
     const unsigned small_grid = (unsigned)c->sms * 4;
@@ -386,7 +386,7 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
     P.passes = (bits + 7) / 8;
     if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && !c->bulk_disabled &&
-        (c->dim == 64 || c->dim == 192)) {
+        (c->dim == 64 || c->dim == 192) && c->n % 8 == 0) {
         int r = c->dim == 64 ? run_bulk_t<64>(c, P) : run_bulk_t<192>(c, P);
         if (r != 1) return r;
         // falls through: P.qlist = heavy queries
@@ -902,7 +902,7 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
     RET(launch_units(c, d_frame, H, W, C, c->units[us].as<float>(), nullptr,
                      temporal ? c->units[us ^ 1].as<float>() : nullptr, temporal ? c->tc.as<double>() : nullptr));
     // K2: queries
-    CK(cudaMemsetAsync(c->stats.p, 0, 48, c->stream));
+    CK(cudaMemsetAsync(c->stats.p, 0, 64, c->stream));
     CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
     rb::QueryParams P;
     memset(&P, 0, sizeof P);
@@ -972,9 +972,9 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         c->prev_units_rows = Q;
     }
     if ((flags & RIANN_F_ASYNC) && dev) return 0;
-    unsigned long long hs[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long hs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     double tcv = 0.0;
-    CK(cudaMemcpyAsync(hs, c->stats.p, 48, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(hs, c->stats.p, 64, cudaMemcpyDeviceToHost, c->stream));
     if (temporal && Q > 0) CK(cudaMemcpyAsync(&tcv, c->tc_sum.p, 8, cudaMemcpyDeviceToHost, c->stream));
     RET(check_err(c));
     if (stats) {
@@ -986,6 +986,7 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         stats->temporal_change = tcv;
         stats->sum_ring_tests = hs[4];
         stats->sum_exact_evals = hs[5];
+        stats->queries_fallback = hs[6];
     }
     return 0;
 }

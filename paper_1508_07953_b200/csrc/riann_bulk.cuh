@@ -303,22 +303,68 @@ __global__ void bulk_scatter_kernel(BulkParams P)
 }
 
 // ---------------------------------------------------------------------------
-// Ring phase: CTA per work item (PH_CHUNK consecutive grouped queries); the
-// anchor's rank row lives in shared memory while its queries are filtered.
+// Ring phase: CTA per work item (PH_CHUNK consecutive grouped queries).  For
+// each run of queries sharing an anchor, one thread starts a TMA bulk copy of
+// the anchor's rank row into shared memory; meanwhile every warp does its
+// queries' row-independent work (state, exact d_a, window search on the sorted
+// row); then the candidate lists are filtered against the shared row.
+__device__ __forceinline__ uint32_t smem_addr(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+struct RingWork {
+    int64_t lo, hi;
+};
+
 template <int D>
 __global__ void __launch_bounds__(PH_WARPS * 32, 1) bulk_ring_kernel(BulkParams P)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint16_t *prow = reinterpret_cast<uint16_t *>(smem_raw);                       // n entries
-    float *crow = reinterpret_cast<float *>(smem_raw + ((P.n * 2 + 15) & ~15LL));  // ncoarse
-    float *rrow = crow + ((P.ncoarse + 3) & ~3);                                   // D floats
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint16_t *prow = reinterpret_cast<uint16_t *>(smem_raw);  // n entries (TMA destination)
+    __shared__ uint64_t bar;
     __shared__ int s_item, s_run_end;
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const int64_t n = P.n;
+    const unsigned row_bytes = (unsigned)(n * 2);
     const int m = *P.n_active_in;
     const int nitems = (m + PH_CHUNK - 1) / PH_CHUNK;
-    const uint64_t pol_keep = pol_evict_last();
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned parity = 0;
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(P.item_next, 1);
         __syncthreads();
@@ -327,130 +373,136 @@ __global__ void __launch_bounds__(PH_WARPS * 32, 1) bulk_ring_kernel(BulkParams 
         const int e0 = item * PH_CHUNK, e1 = min(m, e0 + PH_CHUNK);
         int run0 = e0;
         while (run0 < e1) {
-            // run of equal anchors
             const int a = P.st[P.grouped[run0]].anchor;
             if (threadIdx.x == 0) {
                 int r = run0 + 1;
                 while (r < e1 && P.st[P.grouped[r]].anchor == a) r++;
                 s_run_end = r;
-            }
-            // load the anchor's rank row, coarse row and reference row
-            {
-                const uint4 *src = reinterpret_cast<const uint4 *>(P.pos + (int64_t)a * n);
-                uint4 *dst = reinterpret_cast<uint4 *>(prow);
-                const int nv = (int)(n / 8);
-                for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = __ldcs(src + i);
-                for (int i = nv * 8 + threadIdx.x; i < n; i += blockDim.x) prow[i] = P.pos[(int64_t)a * n + i];
-                for (int i = threadIdx.x; i < P.ncoarse; i += blockDim.x)
-                    crow[i] = P.coarse[(int64_t)a * P.ncoarse + i];
-                for (int i = threadIdx.x; i < D; i += blockDim.x) rrow[i] = P.refs[(int64_t)a * D + i];
+                // the previous run's generic reads of prow are complete (barrier below)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bar, row_bytes);
+                tma_bulk_g2s(prow, P.pos + (int64_t)a * n, row_bytes, &bar);
             }
             __syncthreads();
             const int run1 = s_run_end;
-            for (int e = run0 + w; e < run1; e += PH_WARPS) {
-                const int64_t g = P.grouped[e];
-                QState s = P.st[g];
-                const float *q = P.units + g * D;
-                // search.py:131-133: exact d_a (numpy order), window on row a
-                double da;
-                {
-                    const int gl = lane % Lay<D>::G;
-                    const int base = Lay<D>::base(gl);
-                    double acc = sqdiff(rrow[base], __ldg(q + base));
+            // each warp owns queries run0 + w, run0 + w + PH_WARPS, ...; do the
+            // row-independent part for up to two of them before the row lands
+            for (int eb = run0; eb < run1; eb += 2 * PH_WARPS) {
+                int64_t gq[2];
+                QState sq[2];
+                RingWork rw[2];
+                double dq[2];
 #pragma unroll
-                    for (int i = 1; i < Lay<D>::PER; i++) acc = __dadd_rn(acc, sqdiff(rrow[base + 8 * i], __ldg(q + base + 8 * i)));
-                    acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
-                    acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
-                    acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
-                    if (Lay<D>::G == 16) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 8));
-                    da = __dsqrt_rn(acc);
-                }
-                int64_t lo, hi;
-                window_coarse(P.sdist + (int64_t)a * n, crow, P.ncoarse, n, __dsub_rn(da, __dmul_rn(P.alpha, da)),
-                              __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
-                // search.py:134: S' = S n ring, order kept, filtered in place
-                uint16_t *slot = P.pool + g * LIGHT_MAX;
-                const int cS = s.cS;
-                int nh = 0;
-                for (int base = 0; base < cS; base += 256) {
-                    const int i0 = base + lane * 8;
-                    uint4 v = make_uint4(0, 0, 0, 0);
-                    if (i0 < cS) v = *reinterpret_cast<const uint4 *>(slot + i0);
-                    const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
-                    unsigned keepm = 0;
-#pragma unroll
-                    for (int k = 0; k < 8; k++) {
-                        if (i0 + k < cS) {
-                            const int pk = prow[e8[k]];
-                            if (pk >= lo && pk < hi) keepm |= 1u << k;
-                        }
+                for (int u = 0; u < 2; u++) {
+                    const int e = eb + w + u * PH_WARPS;
+                    gq[u] = e < run1 ? (int64_t)P.grouped[e] : -1;
+                    if (gq[u] >= 0) {
+                        sq[u] = P.st[gq[u]];
+                        const float *q = P.units + gq[u] * D;
+                        const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
+                        dq[u] = da;
+                        window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
+                                      __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)),
+                                      lane, rw[u].lo, rw[u].hi);
                     }
-                    const int kc = __popc(keepm);
-                    const int inc = warp_incl_scan(kc, lane);
-                    const int tot = __shfl_sync(FULL, inc, 31);
-                    __syncwarp();
-                    if (tot > 0) {
-                        int o = nh + inc - kc;
-#pragma unroll
-                        for (int k = 0; k < 8; k++)
-                            if ((keepm >> k) & 1u) slot[o++] = e8[k];
-                    }
-                    nh += tot;
-                    __syncwarp();
                 }
-                if (lane == 0) {
-                    s.tests += cS;
-                    s.exact += 1;
-                    s.rings += 1;
-                    if (nh == 0) {
-                        s.status = ST_DONE;  // search.py:136-137 rollback
-                    } else {
-                        s.cS = nh;
-                        // used anchors still in S
-                        int nu = 0;
-                        for (int i = 0; i < s.nu; i++) {
-                            const int pk = prow[s.u[i]];
-                            if (pk >= lo && pk < hi) s.u[nu++] = s.u[i];
+                if (eb == run0) mbar_wait(&bar, parity);
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    if (gq[u] < 0) continue;
+                    const int64_t g = gq[u];
+                    QState &s = sq[u];
+                    const int64_t lo = rw[u].lo, hi = rw[u].hi;
+                    // search.py:134: S' = S n ring, order kept, filtered in place
+                    uint16_t *slot = P.pool + g * LIGHT_MAX;
+                    const int cS = s.cS;
+                    int nh = 0;
+                    for (int base = 0; base < cS; base += 2048) {
+                        uint4 v[8];
+#pragma unroll
+                        for (int k = 0; k < 8; k++) {
+                            const int i0 = base + k * 256 + lane * 8;
+                            v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
                         }
-                        s.nu = nu;
-                        bool pin = false;
-                        for (int i = 0; i < nu; i++) pin |= s.u[i] == P.prev[g];
-                        s.p_in = pin;
-                        s.status = ST_DONE;
-                        if (nh >= P.L && s.rings < P.max_rings && nh - nu > 0) {
-                            int upos[BULK_U];
-                            for (int i = 0; i < nu; i++) upos[i] = lower_bound_u16(slot, nh, (uint32_t)s.u[i]);
-                            Pcg64 rng;
-                            rng_load(rng, s);
-                            const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
-                            const int pos = avail_pos(k, upos, nu);
-                            if (nu >= BULK_U) {
-                                s.status = ST_HEAVY;
-                                P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
-                            } else {
-                                s.anchor = (int)slot[pos];
-                                s.u[s.nu++] = s.anchor;
-                                rng_store(s, rng);
-                                s.status = ST_ACTIVE;
-                                P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+                        __syncwarp();
+#pragma unroll
+                        for (int k = 0; k < 8; k++) {
+                            const int i0 = base + k * 256 + lane * 8;
+                            if (!__any_sync(FULL, i0 < cS)) break;
+                            const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
+                            unsigned keepm = 0;
+#pragma unroll
+                            for (int x = 0; x < 8; x++) {
+                                if (i0 + x < cS) {
+                                    const int pk = prow[e8[x]];
+                                    if (pk >= lo && pk < hi) keepm |= 1u << x;
+                                }
+                            }
+                            const int kc = __popc(keepm);
+                            const int inc = warp_incl_scan(kc, lane);
+                            const int tot = __shfl_sync(FULL, inc, 31);
+                            int o = nh + inc - kc;
+#pragma unroll
+                            for (int x = 0; x < 8; x++)
+                                if ((keepm >> x) & 1u) slot[o++] = e8[x];
+                            nh += tot;
+                        }
+                        __syncwarp();
+                    }
+                    if (lane == 0) {
+                        s.tests += cS;
+                        s.exact += 1;
+                        s.rings += 1;
+                        if (nh == 0) {
+                            s.status = ST_DONE;  // search.py:136-137 rollback
+                        } else {
+                            s.cS = nh;
+                            int nu = 0;
+                            for (int i = 0; i < s.nu; i++) {
+                                const int pk = prow[s.u[i]];
+                                if (pk >= lo && pk < hi) s.u[nu++] = s.u[i];
+                            }
+                            s.nu = nu;
+                            bool pin = false;
+                            for (int i = 0; i < nu; i++) pin |= s.u[i] == P.prev[g];
+                            s.p_in = pin;
+                            s.status = ST_DONE;
+                            if (nh >= P.L && s.rings < P.max_rings && nh - nu > 0) {
+                                int upos[BULK_U];
+                                for (int i = 0; i < nu; i++) upos[i] = lower_bound_u16(slot, nh, (uint32_t)s.u[i]);
+                                Pcg64 rng;
+                                rng_load(rng, s);
+                                const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
+                                const int pos = avail_pos(k, upos, nu);
+                                if (nu >= BULK_U) {
+                                    s.status = ST_HEAVY;
+                                    P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
+                                } else {
+                                    s.anchor = (int)slot[pos];
+                                    s.u[s.nu++] = s.anchor;
+                                    rng_store(s, rng);
+                                    s.status = ST_ACTIVE;
+                                    P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+                                }
                             }
                         }
+                        P.st[g] = s;
                     }
-                    P.st[g] = s;
+                    __syncwarp();
+                    (void)dq;
                 }
-                __syncwarp();
             }
+            parity ^= 1u;
             __syncthreads();
             run0 = run1;
         }
     }
-    (void)pol_keep;
 }
 
 // ---------------------------------------------------------------------------
 // F: final scan of S u {prev} for every light query (status DONE).
 template <int D>
-__global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P)
+__global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P)
 {
     constexpr int GX = Lay<D>::G;
     constexpr int NGX = WARP / GX;
@@ -509,28 +561,60 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P)
             nsv = 0;
             __syncwarp();
         };
-        for (int e0 = 0; e0 < cS; e0 += 4) {
-            const int e = e0 + grp8;
-            const bool valid = e < cS;
-            const uint32_t j = slot[valid ? e : 0];
-            const float s = approx_sq<D>(P.refs16 + (int64_t)j * D, qs, l8, pol_keep);
-            const float e16 = ld_keep(P.err16 + j, pol_keep);
-            const float ub = __fadd_ru(__fsqrt_ru(__fmul_ru(s, 1.00001f)), __fadd_ru(e16, 1e-12f));
-            const float lb = __fsub_rd(__fsqrt_rd(__fmul_rd(s, 0.99999f)), __fadd_ru(e16, 1e-12f));
-            float mv = valid ? ub : ub_min;
-            mv = fminf(mv, __shfl_xor_sync(FULL, mv, 8));
-            mv = fminf(mv, __shfl_xor_sync(FULL, mv, 16));
-            ub_min = fminf(ub_min, mv);
-            const bool surv = valid && l8 == 0 && lb <= ub_min;
-            const unsigned ball = __ballot_sync(FULL, surv);
-            const int add = __popc(ball);
-            if (nsv + add > SURV_CAP) flush();
-            if (surv) {
-                const int slot2 = nsv + __popc(ball & lanemask_lt());
-                sv_j[slot2] = j;
-                sv_lb[slot2] = lb;
+        for (int e0 = 0; e0 < cS; e0 += 16) {
+            // 4 candidates per 8-lane group in flight
+            uint32_t j[4];
+            uint4 v[4][Scr<D>::NV];
+            float e16[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * 4 + grp8;
+                j[u] = slot[e < cS ? e : 0];
             }
-            nsv += add;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint4 *rp = reinterpret_cast<const uint4 *>(P.refs16 + (int64_t)j[u] * D) + l8;
+#pragma unroll
+                for (int mm = 0; mm < Scr<D>::NV; mm++) v[u][mm] = ld_keep16(rp + mm * 8, pol_keep);
+                e16[u] = ld_keep(P.err16 + j[u], pol_keep);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * 4 + grp8;
+                const bool valid = e < cS;
+                float acc = 0.f;
+#pragma unroll
+                for (int mm = 0; mm < Scr<D>::NV; mm++) {
+                    const __half2 *h2 = reinterpret_cast<const __half2 *>(&v[u][mm]);
+#pragma unroll
+                    for (int x = 0; x < 4; x++) {
+                        const float2 f = __half22float2(h2[x]);
+                        const float d0 = __fsub_rn(f.x, qs[mm * 8 + 2 * x]);
+                        const float d1 = __fsub_rn(f.y, qs[mm * 8 + 2 * x + 1]);
+                        acc = __fmaf_rn(d0, d0, acc);
+                        acc = __fmaf_rn(d1, d1, acc);
+                    }
+                }
+                acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
+                acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
+                acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
+                const float ub = __fadd_ru(__fsqrt_ru(__fmul_ru(acc, 1.00001f)), __fadd_ru(e16[u], 1e-12f));
+                const float lb = __fsub_rd(__fsqrt_rd(__fmul_rd(acc, 0.99999f)), __fadd_ru(e16[u], 1e-12f));
+                float mv = valid ? ub : ub_min;
+                mv = fminf(mv, __shfl_xor_sync(FULL, mv, 8));
+                mv = fminf(mv, __shfl_xor_sync(FULL, mv, 16));
+                ub_min = fminf(ub_min, mv);
+                const bool surv = valid && l8 == 0 && lb <= ub_min;
+                const unsigned ball = __ballot_sync(FULL, surv);
+                const int add = __popc(ball);
+                if (nsv + add > SURV_CAP) flush();
+                if (surv) {
+                    const int slot2 = nsv + __popc(ball & lanemask_lt());
+                    sv_j[slot2] = j[u];
+                    sv_lb[slot2] = lb;
+                }
+                nsv += add;
+            }
         }
         flush();
         warp_argmin(bd, bi);

@@ -762,6 +762,7 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
         atomicAdd(P.stats + 3, acc_f);
         atomicAdd(P.stats + 4, acc_t);
         atomicAdd(P.stats + 5, acc_x);
+        if (P.qlist && gwarp == 0) atomicAdd(P.stats + 6, (unsigned long long)qn);
     }
 }
 

@@ -32,5 +32,5 @@ for t, (_, fld, st) in enumerate(it):
     Q = st.queries
     print(f"frame {t+1}: {1e3*(now-last):.1f} ms  {Q/(now-last)/1e6:.2f} Mq/s  evals/q {st.total_distance_evals/Q:.1f} "
           f"rings/q {st.total_rings/Q:.2f} W1/q {st.first_ring_total/Q:.1f} candF {st.mean_candidates:.1f} "
-          f"tests/q {st.ring_tests_total/Q:.0f} exact/q {st.exact_evals_total/Q:.2f}", flush=True)
+          f"tests/q {st.ring_tests_total/Q:.0f} exact/q {st.exact_evals_total/Q:.2f} heavy {st.fallback_queries/Q*100:.1f}%", flush=True)
     last = now

@@ -179,7 +179,7 @@ struct riann_ctx {
     int ncoarse = 0;
     bool bulk_disabled = false;
     // bulk-path frame buffers
-    DevBuf b_state, b_pool, b_active[2], b_heavy, b_counters, b_counts, b_starts, b_grouped, b_scan_tmp;
+    DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_counters, b_counts, b_starts, b_grouped, b_scan_tmp;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -263,7 +263,10 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
 {
     const int64_t QN = Pq.Q, n = c->n;
     RET(c->b_state.ensure((size_t)QN * sizeof(rb::QState)));
-    RET(c->b_pool.ensure((size_t)QN * rb::LIGHT_MAX * 2));
+    // candidate pool: sum of first-ring sizes, capped (overflowing queries fall back to K2)
+    const size_t pool_entries = std::min<size_t>((size_t)QN * 2048, (size_t)6 << 30);
+    RET(c->b_pool.ensure(pool_entries * 2));
+    RET(c->b_p0spill.ensure((size_t)c->sms * 8 * 8 * 2 * rb::LIGHT_MAX * 2));
     RET(c->b_active[0].ensure((size_t)QN * 4));
     RET(c->b_active[1].ensure((size_t)QN * 4));
     RET(c->b_heavy.ensure((size_t)QN * 4));
@@ -275,7 +278,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, c->b_counts.as<int32_t>(), c->b_starts.as<int32_t>(),
                                      (int)(n + 1), c->stream));
     RET(c->b_scan_tmp.ensure(scan_bytes));
-    int32_t *ctr = c->b_counters.as<int32_t>();  // [0..1] active counts, [2] heavy, [3] item counter
+    int32_t *ctr = c->b_counters.as<int32_t>();  // [0..1] active counts, [2] heavy, [3] item counter, [4..5] pool top
     CK(cudaMemsetAsync(ctr, 0, 64, c->stream));
 
     rb::BulkParams B;
@@ -304,6 +307,9 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.passes = Pq.passes;
     B.st = c->b_state.as<rb::QState>();
     B.pool = c->b_pool.as<uint16_t>();
+    B.pool_top = reinterpret_cast<unsigned long long *>(ctr + 4);
+    B.pool_cap = (int64_t)pool_entries;
+    B.p0_spill = c->b_p0spill.as<uint16_t>();
     B.heavy = c->b_heavy.as<int32_t>();
     B.n_heavy = ctr + 2;
     B.counts = c->b_counts.as<int32_t>();
@@ -318,12 +324,12 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     // P0
     {
         const int wpb = 8;
-        const size_t smem = (size_t)wpb * (2 * rb::LIGHT_MAX * 2 + 1024);
+        const size_t smem = (size_t)wpb * rb::K2_SMEM_BYTES;
         auto k = rb::bulk_p0_kernel<D>;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int bps = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, wpb * 32, smem));
-        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::max(bps, 1), (QN + wpb - 1) / wpb);
+        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::min(std::max(bps, 1), 8), (QN + wpb - 1) / wpb);
         B.active_out = c->b_active[0].as<int32_t>();
         B.n_active_out = ctr + 0;
         k<<<(unsigned)std::max<int64_t>(blocks, 1), wpb * 32, smem, c->stream>>>(B);
@@ -616,7 +622,7 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_grouped, &c->b_scan_tmp, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
+                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
                       &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,

@@ -23,7 +23,7 @@
 
 namespace rb {
 
-constexpr int LIGHT_MAX = 2048;  // candidate slot size (u16 entries) = smem list capacity
+constexpr int LIGHT_MAX = 16384;  // largest first ring handled by the bulk path (u16 entries)
 constexpr int BULK_U = 4;        // used anchors tracked per query
 constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 constexpr int PH_WARPS = 16;     // warps per ring-phase CTA
@@ -33,6 +33,7 @@ enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
 
 struct __align__(16) QState {
     double d_prev;
+    int64_t s_off;            // candidate slot offset in the pool
     uint64_t sh, sl, ih, il;  // PCG64 state and increment
     int32_t cS, first, rings, status;
     int32_t anchor, nu, rng_has, p_in;
@@ -63,7 +64,10 @@ struct BulkParams {
     int max_rings;
     int passes;
     QState *st;
-    uint16_t *pool;          // Q * LIGHT_MAX candidate slots
+    uint16_t *pool;          // candidate slots (variable size, atomic allocation)
+    unsigned long long *pool_top;
+    int64_t pool_cap;
+    uint16_t *p0_spill;      // per P0 warp: 2 * LIGHT_MAX entries
     int32_t *active_in;      // queries whose anchor is pending (this phase)
     const int32_t *n_active_in;
     int32_t *active_out;     // next phase
@@ -202,13 +206,15 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
-    unsigned char *ws = smem_raw + (size_t)wib * (2 * LIGHT_MAX * 2 + 1024);
-    uint32_t *hist = reinterpret_cast<uint32_t *>(ws + 4 * LIGHT_MAX);
+    unsigned char *ws = smem_raw + (size_t)wib * K2_SMEM_BYTES;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(ws + 2 * LIST_BYTES);
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const int64_t n = P.n;
-    for (int64_t g = (int64_t)blockIdx.x * wpb + wib; g < P.Q; g += nwarps) {
-        QList<uint16_t> A{reinterpret_cast<uint16_t *>(ws), nullptr};
-        QList<uint16_t> B{reinterpret_cast<uint16_t *>(ws + 2 * LIGHT_MAX), nullptr};
+    const int64_t gwarp = (int64_t)blockIdx.x * wpb + wib;
+    uint16_t *spill = P.p0_spill + gwarp * 2 * LIGHT_MAX;
+    for (int64_t g = gwarp; g < P.Q; g += nwarps) {
+        QList<uint16_t> A{reinterpret_cast<uint16_t *>(ws), spill};
+        QList<uint16_t> B{reinterpret_cast<uint16_t *>(ws + LIST_BYTES), spill + LIGHT_MAX};
         const float *q = P.units + g * D;
         const int p = P.prev[g];
         QState s;
@@ -223,7 +229,13 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
         window_coarse(P.sdist + (int64_t)p * n, P.coarse + (int64_t)p * P.ncoarse, P.ncoarse, n,
                       __dsub_rn(d, __dmul_rn(P.alpha, d)), __dadd_rn(d, __dmul_rn(P.alpha, d)), lane, lo, hi);
         const int cS = (int)(hi - lo);
-        if (cS > LIGHT_MAX) {
+        int64_t off = 0;
+        if (lane == 0 && cS <= LIGHT_MAX) {
+            off = (int64_t)atomicAdd(P.pool_top, (unsigned long long)((cS + 7) & ~7));
+            if (off + cS > P.pool_cap) off = -1;
+        }
+        off = __shfl_sync(FULL, off, 0);
+        if (cS > LIGHT_MAX || off < 0) {
             if (lane == 0) {
                 P.st[g].status = ST_HEAVY;
                 P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
@@ -233,22 +245,20 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
         bool p_in = false;
         for (int64_t k = lo + lane; k < hi; k += 32) {
             const uint32_t j = __ldg(P.sidx + (int64_t)p * n + k);
-            A.sm[k - lo] = (uint16_t)j;
+            A.put((int)(k - lo), j);
             p_in |= (j == (uint32_t)p);
         }
         p_in = __any_sync(FULL, p_in);
+        __threadfence_block();
         __syncwarp();
         const bool loop = cS >= P.L && P.max_rings > 1;
         if (loop) warp_radix_sort(A, B, cS, P.passes, hist, lane);
-        // candidate slot (16-byte aligned): g * LIGHT_MAX
-        uint16_t *slot = P.pool + g * LIGHT_MAX;
-        {
-            const uint4 *src = reinterpret_cast<const uint4 *>(A.sm);
-            uint4 *dst = reinterpret_cast<uint4 *>(slot);
-            for (int i = lane; i < (cS + 7) / 8; i += 32) dst[i] = src[i];
-        }
+        uint16_t *slot = P.pool + off;
+        for (int i = lane; i < cS; i += 32) slot[i] = (uint16_t)A.get(i);
+        __syncwarp();
         if (lane == 0) {
             s.d_prev = d;
+            s.s_off = off;
             s.cS = cS;
             s.first = cS;
             s.rings = 1;
@@ -262,7 +272,7 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             int upos[BULK_U];
             if (p_in) {
                 s.u[0] = p;
-                upos[0] = lower_bound_u16(A.sm, cS, (uint32_t)p);
+                upos[0] = lower_bound_u16(slot, cS, (uint32_t)p);
                 s.nu = 1;
             }
             if (loop && cS - s.nu > 0) {
@@ -270,7 +280,7 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
                 seed_frame(rng, P, g);
                 const int k = (int)pcg_integers(rng, (uint64_t)(cS - s.nu));
                 const int pos = avail_pos(k, upos, s.nu);
-                s.anchor = (int)A.sm[pos];
+                s.anchor = (int)slot[pos];
                 s.u[s.nu++] = s.anchor;
                 rng_store(s, rng);
                 s.status = ST_ACTIVE;
@@ -414,7 +424,7 @@ __global__ void __launch_bounds__(PH_WARPS * 32, 1) bulk_ring_kernel(BulkParams 
                     QState &s = sq[u];
                     const int64_t lo = rw[u].lo, hi = rw[u].hi;
                     // search.py:134: S' = S n ring, order kept, filtered in place
-                    uint16_t *slot = P.pool + g * LIGHT_MAX;
+                    uint16_t *slot = P.pool + s.s_off;
                     const int cS = s.cS;
                     int nh = 0;
                     for (int base = 0; base < cS; base += 2048) {
@@ -525,7 +535,7 @@ __global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P)
         const int p = P.prev[g];
         const double d = sr.d_prev;
         const float *q = P.units + g * D;
-        const uint16_t *slot = P.pool + g * LIGHT_MAX;
+        const uint16_t *slot = P.pool + sr.s_off;
         double bd = d;
         int bi = p;
         long long exact_cnt = sr.exact;

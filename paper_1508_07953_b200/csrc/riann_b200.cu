@@ -264,7 +264,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     const int64_t QN = Pq.Q, n = c->n;
     RET(c->b_state.ensure((size_t)QN * sizeof(rb::QState)));
     // candidate pool: sum of first-ring sizes, capped (overflowing queries fall back to K2)
-    const size_t pool_entries = std::min<size_t>((size_t)QN * 2048, (size_t)6 << 30);
+    const size_t pool_entries = std::min<size_t>((size_t)QN * 8192, (size_t)6 << 30);
     RET(c->b_pool.ensure(pool_entries * 2));
     RET(c->b_p0spill.ensure((size_t)c->sms * 8 * 8 * 2 * rb::LIGHT_MAX * 2));
     RET(c->b_active[0].ensure((size_t)QN * 4));
@@ -337,9 +337,10 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         c->launches += 1;
     }
     // ring phases
-    const size_t ring_smem = ((size_t)n * 2 + 127) & ~(size_t)127;
     auto rk = rb::bulk_ring_kernel<D>;
-    CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem));
+    int ring_bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ring_bps, rk, 256, 0));
+    const unsigned ring_grid = (unsigned)(c->sms * std::max(ring_bps, 1));
     const unsigned small_grid = (unsigned)c->sms * 4;
     const int phases = Pq.max_rings - 1;
     for (int ph = 0; ph < phases; ph++) {
@@ -363,7 +364,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
-        rk<<<(unsigned)c->sms, rb::PH_WARPS * 32, ring_smem, c->stream>>>(B);
+        rk<<<ring_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
         c->launches += 3;
     }

@@ -355,157 +355,97 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigne
         : "memory");
 }
 
-struct RingWork {
-    int64_t lo, hi;
-};
-
+// ---------------------------------------------------------------------------
+// Ring phase: one warp per (query, anchor), queries taken in anchor order so
+// the ~200 anchor rank rows in flight at any time stay resident in L2 (a row
+// is read from HBM about once per phase); membership tests are 8-deep
+// independent lookups pos[a][j] per lane.
 template <int D>
-__global__ void __launch_bounds__(PH_WARPS * 32, 1) bulk_ring_kernel(BulkParams P)
+__global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
 {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint16_t *prow = reinterpret_cast<uint16_t *>(smem_raw);  // n entries (TMA destination)
-    __shared__ uint64_t bar;
-    __shared__ int s_item, s_run_end;
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t n = P.n;
-    const unsigned row_bytes = (unsigned)(n * 2);
     const int m = *P.n_active_in;
-    const int nitems = (m + PH_CHUNK - 1) / PH_CHUNK;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    unsigned parity = 0;
-    for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(P.item_next, 1);
-        __syncthreads();
-        const int item = s_item;
-        if (item >= nitems) break;
-        const int e0 = item * PH_CHUNK, e1 = min(m, e0 + PH_CHUNK);
-        int run0 = e0;
-        while (run0 < e1) {
-            const int a = P.st[P.grouped[run0]].anchor;
-            if (threadIdx.x == 0) {
-                int r = run0 + 1;
-                while (r < e1 && P.st[P.grouped[r]].anchor == a) r++;
-                s_run_end = r;
-                // the previous run's generic reads of prow are complete (barrier below)
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&bar, row_bytes);
-                tma_bulk_g2s(prow, P.pos + (int64_t)a * n, row_bytes, &bar);
-            }
-            __syncthreads();
-            const int run1 = s_run_end;
-            // each warp owns queries run0 + w, run0 + w + PH_WARPS, ...; do the
-            // row-independent part for up to two of them before the row lands
-            for (int eb = run0; eb < run1; eb += 2 * PH_WARPS) {
-                int64_t gq[2];
-                QState sq[2];
-                RingWork rw[2];
-                double dq[2];
+    for (int64_t i = gwarp; i < m; i += nwarps) {
+        const int64_t g = P.grouped[i];
+        QState s = P.st[g];
+        const int a = s.anchor;
+        const float *q = P.units + g * D;
+        // search.py:131-133: exact d_a (numpy order), window on row a
+        const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
+        int64_t lo, hi;
+        window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
+                      __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
+        const uint16_t *prow = P.pos + (int64_t)a * n;
+        // search.py:134: S' = S n ring, order kept, filtered in place
+        uint16_t *slot = P.pool + s.s_off;
+        const int cS = s.cS;
+        int nh = 0;
+        for (int base = 0; base < cS; base += 256) {
+            const int i0 = base + lane * 8;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (i0 < cS) v = *reinterpret_cast<const uint4 *>(slot + i0);
+            const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
+            uint16_t pk[8];
 #pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    const int e = eb + w + u * PH_WARPS;
-                    gq[u] = e < run1 ? (int64_t)P.grouped[e] : -1;
-                    if (gq[u] >= 0) {
-                        sq[u] = P.st[gq[u]];
-                        const float *q = P.units + gq[u] * D;
-                        const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
-                        dq[u] = da;
-                        window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
-                                      __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)),
-                                      lane, rw[u].lo, rw[u].hi);
-                    }
-                }
-                if (eb == run0) mbar_wait(&bar, parity);
+            for (int x = 0; x < 8; x++) pk[x] = (i0 + x < cS) ? __ldg(prow + e8[x]) : (uint16_t)0xffff;
+            unsigned keepm = 0;
 #pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    if (gq[u] < 0) continue;
-                    const int64_t g = gq[u];
-                    QState &s = sq[u];
-                    const int64_t lo = rw[u].lo, hi = rw[u].hi;
-                    // search.py:134: S' = S n ring, order kept, filtered in place
-                    uint16_t *slot = P.pool + s.s_off;
-                    const int cS = s.cS;
-                    int nh = 0;
-                    for (int base = 0; base < cS; base += 2048) {
-                        uint4 v[8];
+            for (int x = 0; x < 8; x++)
+                if (i0 + x < cS && pk[x] >= lo && pk[x] < hi) keepm |= 1u << x;
+            const int kc = __popc(keepm);
+            const int inc = warp_incl_scan(kc, lane);
+            const int tot = __shfl_sync(FULL, inc, 31);
+            __syncwarp();
+            int o = nh + inc - kc;
 #pragma unroll
-                        for (int k = 0; k < 8; k++) {
-                            const int i0 = base + k * 256 + lane * 8;
-                            v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
-                        }
-                        __syncwarp();
-#pragma unroll
-                        for (int k = 0; k < 8; k++) {
-                            const int i0 = base + k * 256 + lane * 8;
-                            if (!__any_sync(FULL, i0 < cS)) break;
-                            const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
-                            unsigned keepm = 0;
-#pragma unroll
-                            for (int x = 0; x < 8; x++) {
-                                if (i0 + x < cS) {
-                                    const int pk = prow[e8[x]];
-                                    if (pk >= lo && pk < hi) keepm |= 1u << x;
-                                }
-                            }
-                            const int kc = __popc(keepm);
-                            const int inc = warp_incl_scan(kc, lane);
-                            const int tot = __shfl_sync(FULL, inc, 31);
-                            int o = nh + inc - kc;
-#pragma unroll
-                            for (int x = 0; x < 8; x++)
-                                if ((keepm >> x) & 1u) slot[o++] = e8[x];
-                            nh += tot;
-                        }
-                        __syncwarp();
-                    }
-                    if (lane == 0) {
-                        s.tests += cS;
-                        s.exact += 1;
-                        s.rings += 1;
-                        if (nh == 0) {
-                            s.status = ST_DONE;  // search.py:136-137 rollback
-                        } else {
-                            s.cS = nh;
-                            int nu = 0;
-                            for (int i = 0; i < s.nu; i++) {
-                                const int pk = prow[s.u[i]];
-                                if (pk >= lo && pk < hi) s.u[nu++] = s.u[i];
-                            }
-                            s.nu = nu;
-                            bool pin = false;
-                            for (int i = 0; i < nu; i++) pin |= s.u[i] == P.prev[g];
-                            s.p_in = pin;
-                            s.status = ST_DONE;
-                            if (nh >= P.L && s.rings < P.max_rings && nh - nu > 0) {
-                                int upos[BULK_U];
-                                for (int i = 0; i < nu; i++) upos[i] = lower_bound_u16(slot, nh, (uint32_t)s.u[i]);
-                                Pcg64 rng;
-                                rng_load(rng, s);
-                                const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
-                                const int pos = avail_pos(k, upos, nu);
-                                if (nu >= BULK_U) {
-                                    s.status = ST_HEAVY;
-                                    P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
-                                } else {
-                                    s.anchor = (int)slot[pos];
-                                    s.u[s.nu++] = s.anchor;
-                                    rng_store(s, rng);
-                                    s.status = ST_ACTIVE;
-                                    P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
-                                }
-                            }
-                        }
-                        P.st[g] = s;
-                    }
-                    __syncwarp();
-                    (void)dq;
-                }
-            }
-            parity ^= 1u;
-            __syncthreads();
-            run0 = run1;
+            for (int x = 0; x < 8; x++)
+                if ((keepm >> x) & 1u) slot[o++] = e8[x];
+            nh += tot;
+            __syncwarp();
         }
+        if (lane == 0) {
+            s.tests += cS;
+            s.exact += 1;
+            s.rings += 1;
+            if (nh == 0) {
+                s.status = ST_DONE;  // search.py:136-137 rollback
+            } else {
+                s.cS = nh;
+                int nu = 0;
+                for (int k = 0; k < s.nu; k++) {
+                    const int pk = __ldg(prow + s.u[k]);
+                    if (pk >= lo && pk < hi) s.u[nu++] = s.u[k];
+                }
+                s.nu = nu;
+                bool pin = false;
+                for (int k = 0; k < nu; k++) pin |= s.u[k] == P.prev[g];
+                s.p_in = pin;
+                s.status = ST_DONE;
+                if (nh >= P.L && s.rings < P.max_rings && nh - nu > 0) {
+                    int upos[BULK_U];
+                    for (int k = 0; k < nu; k++) upos[k] = lower_bound_u16(slot, nh, (uint32_t)s.u[k]);
+                    Pcg64 rng;
+                    rng_load(rng, s);
+                    const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
+                    const int pos = avail_pos(k, upos, nu);
+                    if (nu >= BULK_U) {
+                        s.status = ST_HEAVY;
+                        P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
+                    } else {
+                        s.anchor = (int)slot[pos];
+                        s.u[s.nu++] = s.anchor;
+                        rng_store(s, rng);
+                        s.status = ST_ACTIVE;
+                        P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+                    }
+                }
+            }
+            P.st[g] = s;
+        }
+        __syncwarp();
     }
 }
 

@@ -243,18 +243,53 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             continue;
         }
         bool p_in = false;
-        for (int64_t k = lo + lane; k < hi; k += 32) {
-            const uint32_t j = __ldg(P.sidx + (int64_t)p * n + k);
-            A.put((int)(k - lo), j);
-            p_in |= (j == (uint32_t)p);
+        {
+            // window of the u16 index row: 16-byte vector loads over the aligned
+            // span, element-wise head and tail
+            const uint16_t *row = P.sidx + (int64_t)p * n;
+            const int64_t a0 = (lo + 7) & ~(int64_t)7, a1 = hi & ~(int64_t)7;
+            if (a0 < a1) {
+                for (int64_t k = lo + lane; k < a0; k += 32) {
+                    const uint32_t j = __ldg(row + k);
+                    A.put((int)(k - lo), j);
+                    p_in |= (j == (uint32_t)p);
+                }
+                for (int64_t v0 = a0 + (int64_t)lane * 8; v0 < a1; v0 += 256) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + v0));
+                    const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
+#pragma unroll
+                    for (int x = 0; x < 8; x++) {
+                        A.put((int)(v0 + x - lo), e8[x]);
+                        p_in |= (e8[x] == (uint16_t)p);
+                    }
+                }
+                for (int64_t k = a1 + lane; k < hi; k += 32) {
+                    const uint32_t j = __ldg(row + k);
+                    A.put((int)(k - lo), j);
+                    p_in |= (j == (uint32_t)p);
+                }
+            } else {
+                for (int64_t k = lo + lane; k < hi; k += 32) {
+                    const uint32_t j = __ldg(row + k);
+                    A.put((int)(k - lo), j);
+                    p_in |= (j == (uint32_t)p);
+                }
+            }
         }
         p_in = __any_sync(FULL, p_in);
         __threadfence_block();
         __syncwarp();
         const bool loop = cS >= P.L && P.max_rings > 1;
         if (loop) warp_radix_sort(A, B, cS, P.passes, hist, lane);
-        uint16_t *slot = P.pool + off;
-        for (int i = lane; i < cS; i += 32) slot[i] = (uint16_t)A.get(i);
+        uint16_t *slot = P.pool + off;  // 16-byte aligned (slots rounded to 8 entries)
+        {
+            const int cap = QList<uint16_t>::CAP;
+            const int nv = (min(cS, cap) + 7) / 8;
+            const uint4 *src = reinterpret_cast<const uint4 *>(A.sm);
+            uint4 *dst = reinterpret_cast<uint4 *>(slot);
+            for (int i = lane; i < nv; i += 32) dst[i] = src[i];
+            for (int i = cap + lane; i < cS; i += 32) slot[i] = (uint16_t)A.get(i);
+        }
         __syncwarp();
         if (lane == 0) {
             s.d_prev = d;
@@ -364,11 +399,22 @@ template <int D>
 __global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
 {
     const int lane = threadIdx.x & 31;
-    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t n = P.n;
     const int m = *P.n_active_in;
-    for (int64_t i = gwarp; i < m; i += nwarps) {
+    // dynamic chunks of consecutive (anchor-ordered) entries keep the set of
+    // queries in flight -- and hence of anchor rows -- a narrow window
+    constexpr int GRAB = 4;
+    int ibase = 0, icnt = 0;
+    for (;;) {
+        if (icnt == 0) {
+            int b = 0;
+            if (lane == 0) b = atomicAdd(P.item_next, GRAB);
+            ibase = __shfl_sync(FULL, b, 0);
+            icnt = GRAB;
+        }
+        const int i = ibase + (GRAB - icnt);
+        icnt--;
+        if (i >= m) break;
         const int64_t g = P.grouped[i];
         QState s = P.st[g];
         const int a = s.anchor;

@@ -50,7 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(REPO, "include"),
-           "-o", tmp, os.path.join(CSRC, "riann_b200.cu")]
+           "-o", tmp, os.path.join(CSRC, "riann_b200.cu"),
+           "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -5,6 +5,7 @@
 // launches K1 (units) -> K2 (query) -> pairwise reduction per frame on the
 // context's stream.  No CPU fallback: every compute entry point runs on the
 // GPU or returns an error.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
@@ -13,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 #include <array>
 #include <cstring>
@@ -176,6 +178,11 @@ struct riann_ctx {
     bool idx16 = false;  // sorted index table stored as uint16 (n <= 65536)
     DevBuf refs, refs16, err16, sdist, sidx, dmat;
     DevBuf pos, coarse;  // rank rows and coarse index (bulk path, n <= 65536)
+    // PCA screening basis (bulk final scan)
+    DevBuf pca_T, refs_pca16, e16p, units_pca, e16max;
+    bool pca = false;
+    float pca_dq = 0.f, pca_eta = 0.f, pca_e16max = 0.f;
+    cublasHandle_t cublas = nullptr;
     int ncoarse = 0;
     bool bulk_disabled = false;
     // bulk-path frame buffers
@@ -215,7 +222,8 @@ struct riann_ctx {
     }
     uint64_t bytes() const
     {
-        uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + pos.cap + coarse.cap + b_state.cap +
+        uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + pos.cap + coarse.cap + b_state.cap + pca_T.cap +
+                     refs_pca16.cap + e16p.cap + units_pca.cap +
                      b_pool.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
                      fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap;
         return b;
@@ -368,13 +376,29 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaGetLastError());
         c->launches += 3;
     }
-    // final scan of the light queries
+    // final scan of the light queries (PCA-basis screening)
     {
+        RET(c->units_pca.ensure((size_t)QN * D * 4));
+        CK(cublasSetStream(c->cublas, c->stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
+        const float one = 1.f, zero = 0.f;
+        if (cublasSgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)QN, D, &one, c->pca_T.as<float>(), D, Pq.units,
+                        D, &zero, c->units_pca.as<float>(), D) != CUBLAS_STATUS_SUCCESS)
+            return fail(RIANN_E_CUDA, "cublasSgemm failed");
+        rb::ScreenParams SP;
+        SP.refs_pca16 = c->refs_pca16.as<__half>();
+        SP.e16p = c->e16p.as<float>();
+        SP.units_pca = c->units_pca.as<float>();
+        SP.dq = c->pca_dq + 1e-12f;
+        SP.slack = c->pca_dq + c->pca_e16max + 2e-12f;
+        SP.one_plus_eta = 1.0f + c->pca_eta * 1.001f;
+        SP.one_minus_eta = 1.0f - c->pca_eta * 1.001f;
         auto k = rb::bulk_final_kernel<D>;
+        const size_t smem = 8 * (2 * rb::FB * 8 + 128 * 8);
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, smem));
         int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::max(bps, 1), (QN + 7) / 8);
-        k<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, c->stream>>>(B);
+        k<<<(unsigned)std::max<int64_t>(blocks, 1), 256, smem, c->stream>>>(B, SP);
         CK(cudaGetLastError());
         c->launches += 1;
     }
@@ -392,7 +416,7 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     int bits = 1;
     while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
     P.passes = (bits + 7) / 8;
-    if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && !c->bulk_disabled &&
+    if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && c->pca && !c->bulk_disabled &&
         (c->dim == 64 || c->dim == 192) && c->n % 8 == 0) {
         int r = c->dim == 64 ? run_bulk_t<64>(c, P) : run_bulk_t<192>(c, P);
         if (r != 1) return r;
@@ -418,6 +442,124 @@ int check_err(riann_ctx *c)
     if (h == rb::ERR_USED_OVERFLOW)
         return fail(RIANN_E_UNSUPPORTED, "more than 32 used anchors remained in the candidate set");
     if (h) return fail(RIANN_E_CUDA, "kernel error %d", h);
+    return 0;
+}
+
+// Cyclic Jacobi eigendecomposition of a symmetric matrix (row-major, dim D):
+// A is destroyed, V receives eigenvectors as columns, w the eigenvalues.
+void jacobi_eigen(std::vector<double> &A, int D, std::vector<double> &V, std::vector<double> &w)
+{
+    V.assign((size_t)D * D, 0.0);
+    for (int i = 0; i < D; i++) V[(size_t)i * D + i] = 1.0;
+    double total = 0.0;
+    for (double x : A) total += x * x;
+    for (int sweep = 0; sweep < 60; sweep++) {
+        double off = 0.0;
+        for (int p = 0; p < D; p++)
+            for (int q = p + 1; q < D; q++) off += A[(size_t)p * D + q] * A[(size_t)p * D + q];
+        if (off <= 1e-24 * total || off == 0.0) break;
+        for (int p = 0; p < D; p++) {
+            for (int q = p + 1; q < D; q++) {
+                const double apq = A[(size_t)p * D + q];
+                if (std::fabs(apq) < 1e-300) continue;
+                const double app = A[(size_t)p * D + p], aqq = A[(size_t)q * D + q];
+                const double theta = (aqq - app) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                for (int k = 0; k < D; k++) {
+                    const double akp = A[(size_t)k * D + p], akq = A[(size_t)k * D + q];
+                    A[(size_t)k * D + p] = cs * akp - sn * akq;
+                    A[(size_t)k * D + q] = sn * akp + cs * akq;
+                }
+                for (int k = 0; k < D; k++) {
+                    const double apk = A[(size_t)p * D + k], aqk = A[(size_t)q * D + k];
+                    A[(size_t)p * D + k] = cs * apk - sn * aqk;
+                    A[(size_t)q * D + k] = sn * apk + cs * aqk;
+                }
+                for (int k = 0; k < D; k++) {
+                    const double vkp = V[(size_t)k * D + p], vkq = V[(size_t)k * D + q];
+                    V[(size_t)k * D + p] = cs * vkp - sn * vkq;
+                    V[(size_t)k * D + q] = sn * vkp + cs * vkq;
+                }
+            }
+        }
+    }
+    w.resize(D);
+    for (int i = 0; i < D; i++) w[i] = A[(size_t)i * D + i];
+}
+
+// PCA screening basis of the references (speed only: any orthogonal basis
+// gives exact results; the bounds account for T's non-orthogonality).
+int build_pca(riann_ctx *c, const float *refs_host)
+{
+    c->pca = false;
+    const int D = c->dim;
+    const int64_t n = c->n;
+    if (!(D == 64 || D == 192)) return 0;
+    const int64_t step = std::max<int64_t>(1, n / 16384);
+    std::vector<double> mu(D, 0.0), C((size_t)D * D, 0.0);
+    int64_t m = 0;
+    for (int64_t j = 0; j < n; j += step, m++)
+        for (int i = 0; i < D; i++) mu[i] += refs_host[j * D + i];
+    for (int i = 0; i < D; i++) mu[i] /= (double)m;
+    std::vector<double> x(D);
+    for (int64_t j = 0; j < n; j += step) {
+        for (int i = 0; i < D; i++) x[i] = refs_host[j * D + i] - mu[i];
+        for (int a = 0; a < D; a++) {
+            const double xa = x[a];
+            double *row = &C[(size_t)a * D];
+            for (int b = a; b < D; b++) row[b] += xa * x[b];
+        }
+    }
+    for (int a = 0; a < D; a++)
+        for (int b = 0; b < a; b++) C[(size_t)a * D + b] = C[(size_t)b * D + a];
+    std::vector<double> V, w;
+    jacobi_eigen(C, D, V, w);
+    std::vector<int> order(D);
+    for (int i = 0; i < D; i++) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return w[a] > w[b]; });
+    std::vector<float> T((size_t)D * D);  // T[k][i]: entry k of basis vector i
+    for (int k = 0; k < D; k++)
+        for (int i = 0; i < D; i++) T[(size_t)k * D + i] = (float)V[(size_t)k * D + order[i]];
+    // eta >= ||T^T T - I||_2 (Frobenius bound, float64)
+    double fro = 0.0;
+    for (int a = 0; a < D; a++)
+        for (int b = 0; b < D; b++) {
+            double dot = 0.0;
+            for (int k = 0; k < D; k++) dot += (double)T[(size_t)k * D + a] * (double)T[(size_t)k * D + b];
+            const double e = dot - (a == b ? 1.0 : 0.0);
+            fro += e * e;
+        }
+    const double eta = std::sqrt(fro) * 1.01 + 1e-12;
+    if (eta > 1e-3) return 0;  // basis too far from orthogonal: skip PCA screening
+    // cuBLAS SGEMM error bound for q' = T^T q, ||q|| <= 1 + 1e-6: per component
+    // gamma_D * sum_k |T_ki q_k| <= gamma_D * ||T_.i|| * ||q||
+    const double u = std::ldexp(1.0, -24), gam = D * u / (1.0 - D * u);
+    const double dq = gam * std::sqrt((double)D) * std::sqrt(1.0 + eta) * (1.0 + 1e-6) * 1.01 + 1e-12;
+    RET(c->pca_T.ensure((size_t)D * D * 4));
+    RET(c->refs_pca16.ensure((size_t)n * D * 2));
+    RET(c->e16p.ensure((size_t)n * 4));
+    RET(c->e16max.ensure(16));
+    CK(cudaMemcpyAsync(c->pca_T.p, T.data(), (size_t)D * D * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->e16max.p, 0, 16, c->stream));
+    rb::refs_pca_kernel<<<(unsigned)((n + 127) / 128), 128, 0, c->stream>>>(
+        c->refs.as<float>(), c->pca_T.as<float>(), n, D, c->refs_pca16.as<__half>(), c->e16p.as<float>(),
+        c->e16max.as<unsigned>());
+    CK(cudaGetLastError());
+    unsigned mx = 0;
+    CK(cudaMemcpyAsync(&mx, c->e16max.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float e16m;
+    memcpy(&e16m, &mx, 4);
+    c->pca_dq = (float)dq;
+    c->pca_eta = (float)eta;
+    c->pca_e16max = e16m;
+    if (!c->cublas) {
+        if (cublasCreate(&c->cublas) != CUBLAS_STATUS_SUCCESS) return fail(RIANN_E_CUDA, "cublasCreate failed");
+        // no TF32 / emulation: the error bound assumes IEEE fp32 FMA dot products
+        cublasSetMathMode(c->cublas, CUBLAS_PEDANTIC_MATH);
+    }
+    c->pca = true;
     return 0;
 }
 
@@ -623,7 +765,8 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
+                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->pca_T, &c->refs_pca16, &c->e16p,
+                      &c->units_pca, &c->e16max, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
                       &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,
@@ -633,6 +776,7 @@ int riann_ctx_destroy(riann_ctx *c)
     for (auto &a : c->ev_pending)
         for (auto e : a) cudaEventDestroy(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->cublas) cublasDestroy(c->cublas);
     cudaStreamDestroy(c->stream);
     delete c;
     return 0;
@@ -686,6 +830,7 @@ int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, in
     CK(cudaStreamSynchronize(c->stream));
     c->n = n;
     c->dim = dim;
+    RET(build_pca(c, refs));
     c->pw = pw;
     c->ph = ph;
     c->C = channels;

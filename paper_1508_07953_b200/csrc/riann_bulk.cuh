@@ -497,48 +497,70 @@ __global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
 
 // ---------------------------------------------------------------------------
 // F: final scan of S u {prev} for every light query (status DONE).
+//
+// Screening in the references' PCA basis: q' = T^T q (cuBLAS SGEMM, pedantic
+// fp32) and r' = fp16(T^T r) (per-row bound e16p[r]).  For T with
+// ||T^T T - I|| <= eta, the true distance d = ||q - r|| satisfies
+//   (||q' - r'|| - dq - e16p[r]) / (1 + eta) <= d <= (||q' - r'|| + dq + e16p[r]) / (1 - eta)
+// (dq bounds the SGEMM rounding error).  Partial sums of squares over the
+// leading 16-component chunks are lower bounds of the full sum, so a candidate
+// is abandoned as soon as its partial lower bound exceeds the best upper bound
+// (initially the previous match's exact distance).  Survivors of all chunks
+// whose lower bound can still reach the minimum get the exact FP64 distance
+// (numpy order), so the first minimum (lowest index on ties) is exact.
+struct ScreenParams {
+    const __half *refs_pca16;  // (n, D) fp16, PCA order
+    const float *e16p;         // per-row bound
+    const float *units_pca;    // (Q, D) fp32
+    float slack;               // dq + max_r e16p[r] + 1e-12 (chunk rejection)
+    float dq;                  // + 1e-12
+    float one_plus_eta, one_minus_eta;
+};
+
+constexpr int FB = 512;  // candidates per screening block
+
 template <int D>
-__global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P)
+__global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, ScreenParams SP)
 {
     constexpr int GX = Lay<D>::G;
     constexpr int NGX = WARP / GX;
-    constexpr int SP = Scr<D>::PER;
+    constexpr int NCH = D / 16;
     constexpr int SURV_CAP = 128;
-    __shared__ __align__(16) uint32_t sv_all[8][2 * SURV_CAP];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
-    uint32_t *sv_j = sv_all[wib];
-    float *sv_lb = reinterpret_cast<float *>(sv_all[wib] + SURV_CAP);
+    // per warp: two (index, partial) lists of FB entries + survivor slots
+    unsigned char *ws = smem_raw + (size_t)wib * (2 * FB * 8 + SURV_CAP * 8);
+    uint32_t *Aj = reinterpret_cast<uint32_t *>(ws);
+    float *As = reinterpret_cast<float *>(ws + FB * 4);
+    uint32_t *Bj = reinterpret_cast<uint32_t *>(ws + FB * 8);
+    float *Bs = reinterpret_cast<float *>(ws + FB * 12);
+    uint32_t *sv_j = reinterpret_cast<uint32_t *>(ws + FB * 16);
+    float *sv_lb = reinterpret_cast<float *>(ws + FB * 16 + SURV_CAP * 4);
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const uint64_t pol_keep = pol_evict_last();
     unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
     for (int64_t g = (int64_t)blockIdx.x * wpb + wib; g < P.Q; g += nwarps) {
         const QState &sr = P.st[g];
-        const int status = sr.status;
-        if (status != ST_DONE) continue;
+        if (sr.status != ST_DONE) continue;
         const int cS = sr.cS;
         const int p = P.prev[g];
         const double d = sr.d_prev;
         const float *q = P.units + g * D;
+        const float *qp = SP.units_pca + g * D;
         const uint16_t *slot = P.pool + sr.s_off;
         double bd = d;
         int bi = p;
         long long exact_cnt = sr.exact;
-        float qs[SP];
-        const int grp8 = lane >> 3, l8 = lane & 7;
-#pragma unroll
-        for (int mm = 0; mm < Scr<D>::NV; mm++)
-#pragma unroll
-            for (int e = 0; e < 8; e++) qs[mm * 8 + e] = __ldg(q + mm * 64 + l8 * 8 + e);
-        float ub_min = __double2float_ru(d);
+        float ub = __double2float_ru(d);
         int nsv = 0;
         auto flush = [&]() {
             __syncwarp();
             int mcount = 0;
             for (int b0 = 0; b0 < nsv; b0 += 32) {
                 const int i = b0 + lane;
-                const bool ok = i < nsv && sv_lb[i] <= ub_min;
+                const bool ok = i < nsv && sv_lb[i] <= ub;
                 const uint32_t jj = i < nsv ? sv_j[i] : 0u;
                 const unsigned ball = __ballot_sync(FULL, ok);
                 __syncwarp();
@@ -557,59 +579,137 @@ __global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P)
             nsv = 0;
             __syncwarp();
         };
-        for (int e0 = 0; e0 < cS; e0 += 16) {
-            // 4 candidates per 8-lane group in flight
-            uint32_t j[4];
-            uint4 v[4][Scr<D>::NV];
-            float e16[4];
+        // partial lower bound in distance space for a partial sum s
+        auto lb_of = [&](float s, float sl) {
+            return __fdiv_rd(__fsub_rd(__fsqrt_rd(__fmul_rd(s, 0.99997f)), sl), SP.one_plus_eta);
+        };
+        for (int blk = 0; blk < cS; blk += FB) {
+            const int bn = min(FB, cS - blk);
+            // chunk 0 over the block, one candidate per lane
+            float qc[16];
+            {
+                const float4 *q4 = reinterpret_cast<const float4 *>(qp);
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int e = e0 + u * 4 + grp8;
-                j[u] = slot[e < cS ? e : 0];
+                for (int k = 0; k < 4; k++) {
+                    const float4 v = __ldg(q4 + k);
+                    qc[4 * k] = v.x;
+                    qc[4 * k + 1] = v.y;
+                    qc[4 * k + 2] = v.z;
+                    qc[4 * k + 3] = v.w;
+                }
             }
+            int nA = 0;
+            for (int e0 = 0; e0 < bn; e0 += 32) {
+                const int e = e0 + lane;
+                const bool valid = e < bn;
+                const uint32_t j = slot[blk + (valid ? e : 0)];
+                const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D);
+                const uint4 v0 = ld_keep16(rp, pol_keep), v1 = ld_keep16(rp + 1, pol_keep);
+                float s = 0.f;
+                const __half2 *h0 = reinterpret_cast<const __half2 *>(&v0);
+                const __half2 *h1 = reinterpret_cast<const __half2 *>(&v1);
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint4 *rp = reinterpret_cast<const uint4 *>(P.refs16 + (int64_t)j[u] * D) + l8;
-#pragma unroll
-                for (int mm = 0; mm < Scr<D>::NV; mm++) v[u][mm] = ld_keep16(rp + mm * 8, pol_keep);
-                e16[u] = ld_keep(P.err16 + j[u], pol_keep);
+                for (int x = 0; x < 4; x++) {
+                    float2 f = __half22float2(h0[x]);
+                    float a0 = __fsub_rn(f.x, qc[2 * x]), a1 = __fsub_rn(f.y, qc[2 * x + 1]);
+                    s = __fmaf_rn(a0, a0, s);
+                    s = __fmaf_rn(a1, a1, s);
+                    f = __half22float2(h1[x]);
+                    a0 = __fsub_rn(f.x, qc[8 + 2 * x]);
+                    a1 = __fsub_rn(f.y, qc[8 + 2 * x + 1]);
+                    s = __fmaf_rn(a0, a0, s);
+                    s = __fmaf_rn(a1, a1, s);
+                }
+                const bool keep = valid && lb_of(s, SP.slack) <= ub;
+                const unsigned ball = __ballot_sync(FULL, keep);
+                if (keep) {
+                    const int o = nA + __popc(ball & lanemask_lt());
+                    Aj[o] = j;
+                    As[o] = s;
+                }
+                nA += __popc(ball);
             }
+            __syncwarp();
+            // further chunks for the candidates still alive
+            for (int c = 1; c < NCH && nA > 0; c++) {
+                {
+                    const float4 *q4 = reinterpret_cast<const float4 *>(qp + 16 * c);
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int e = e0 + u * 4 + grp8;
-                const bool valid = e < cS;
-                float acc = 0.f;
-#pragma unroll
-                for (int mm = 0; mm < Scr<D>::NV; mm++) {
-                    const __half2 *h2 = reinterpret_cast<const __half2 *>(&v[u][mm]);
-#pragma unroll
-                    for (int x = 0; x < 4; x++) {
-                        const float2 f = __half22float2(h2[x]);
-                        const float d0 = __fsub_rn(f.x, qs[mm * 8 + 2 * x]);
-                        const float d1 = __fsub_rn(f.y, qs[mm * 8 + 2 * x + 1]);
-                        acc = __fmaf_rn(d0, d0, acc);
-                        acc = __fmaf_rn(d1, d1, acc);
+                    for (int k = 0; k < 4; k++) {
+                        const float4 v = __ldg(q4 + k);
+                        qc[4 * k] = v.x;
+                        qc[4 * k + 1] = v.y;
+                        qc[4 * k + 2] = v.z;
+                        qc[4 * k + 3] = v.w;
                     }
                 }
-                acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
-                acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
-                acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
-                const float ub = __fadd_ru(__fsqrt_ru(__fmul_ru(acc, 1.00001f)), __fadd_ru(e16[u], 1e-12f));
-                const float lb = __fsub_rd(__fsqrt_rd(__fmul_rd(acc, 0.99999f)), __fadd_ru(e16[u], 1e-12f));
-                float mv = valid ? ub : ub_min;
-                mv = fminf(mv, __shfl_xor_sync(FULL, mv, 8));
-                mv = fminf(mv, __shfl_xor_sync(FULL, mv, 16));
-                ub_min = fminf(ub_min, mv);
-                const bool surv = valid && l8 == 0 && lb <= ub_min;
-                const unsigned ball = __ballot_sync(FULL, surv);
-                const int add = __popc(ball);
-                if (nsv + add > SURV_CAP) flush();
-                if (surv) {
-                    const int slot2 = nsv + __popc(ball & lanemask_lt());
-                    sv_j[slot2] = j[u];
-                    sv_lb[slot2] = lb;
+                const bool last = c == NCH - 1;
+                int nB = 0;
+                for (int i0 = 0; i0 < nA; i0 += 32) {
+                    const int i = i0 + lane;
+                    const bool valid = i < nA;
+                    const uint32_t j = valid ? Aj[i] : Aj[0];
+                    float s = valid ? As[i] : 0.f;
+                    const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D) + 2 * c;
+                    const uint4 v0 = ld_keep16(rp, pol_keep), v1 = ld_keep16(rp + 1, pol_keep);
+                    const __half2 *h0 = reinterpret_cast<const __half2 *>(&v0);
+                    const __half2 *h1 = reinterpret_cast<const __half2 *>(&v1);
+#pragma unroll
+                    for (int x = 0; x < 4; x++) {
+                        float2 f = __half22float2(h0[x]);
+                        float a0 = __fsub_rn(f.x, qc[2 * x]), a1 = __fsub_rn(f.y, qc[2 * x + 1]);
+                        s = __fmaf_rn(a0, a0, s);
+                        s = __fmaf_rn(a1, a1, s);
+                        f = __half22float2(h1[x]);
+                        a0 = __fsub_rn(f.x, qc[8 + 2 * x]);
+                        a1 = __fsub_rn(f.y, qc[8 + 2 * x + 1]);
+                        s = __fmaf_rn(a0, a0, s);
+                        s = __fmaf_rn(a1, a1, s);
+                    }
+                    if (!last) {
+                        const bool keep = valid && lb_of(s, SP.slack) <= ub;
+                        const unsigned ball = __ballot_sync(FULL, keep);
+                        if (keep) {
+                            const int o = nB + __popc(ball & lanemask_lt());
+                            Bj[o] = j;
+                            Bs[o] = s;
+                        }
+                        nB += __popc(ball);
+                    } else {
+                        // complete sums: tighten the upper bound, collect survivors
+                        float e16 = valid ? ld_keep(SP.e16p + j, pol_keep) : 0.f;
+                        const float sl = __fadd_ru(SP.dq, e16);
+                        const float u =
+                            valid ? __fdiv_ru(__fadd_ru(__fsqrt_ru(__fmul_ru(s, 1.00003f)), sl), SP.one_minus_eta)
+                                  : ub;
+                        float mv = u;
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1) mv = fminf(mv, __shfl_xor_sync(FULL, mv, o));
+                        ub = fminf(ub, mv);
+                        const float lb = lb_of(s, sl);
+                        const bool surv = valid && lb <= ub;
+                        const unsigned ball = __ballot_sync(FULL, surv);
+                        const int add = __popc(ball);
+                        if (nsv + add > SURV_CAP) flush();
+                        if (surv) {
+                            const int o = nsv + __popc(ball & lanemask_lt());
+                            sv_j[o] = j;
+                            sv_lb[o] = lb;
+                        }
+                        nsv += add;
+                    }
                 }
-                nsv += add;
+                __syncwarp();
+                if (!last) {
+                    // swap lists
+                    uint32_t *tj = Aj;
+                    float *ts = As;
+                    Aj = Bj;
+                    As = Bs;
+                    Bj = tj;
+                    Bs = ts;
+                    nA = nB;
+                }
             }
         }
         flush();
@@ -635,6 +735,29 @@ __global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P)
         atomicAdd(P.stats + 4, acc_t);
         atomicAdd(P.stats + 5, acc_x);
     }
+}
+
+// r' = fp16(T^T r) per reference row, e16p = rigorous bound of ||r' - T^T r||
+// (T^T r evaluated in float64), and the maximum bound (as float bits).
+__global__ void refs_pca_kernel(const float *refs, const float *T, int64_t n, int dim, __half *out, float *e16,
+                                unsigned *e16max)
+{
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const float *r = refs + j * dim;
+    double acc = 0.0;
+    for (int i = 0; i < dim; i++) {
+        double y = 0.0;
+        for (int k = 0; k < dim; k++) y = fma((double)T[(int64_t)k * dim + i], (double)r[k], y);
+        const __half h = __float2half_rn((float)y);
+        out[j * dim + i] = h;
+        const double dl = (double)__half2float(h) - y;
+        acc = __fma_ru(dl, dl, acc);
+    }
+    // + dim * 1e-15 covers the float64 evaluation error of y
+    const float b = __double2float_ru(__dsqrt_ru(acc) + 1e-13);
+    e16[j] = b;
+    atomicMax(e16max, __float_as_uint(b));
 }
 
 // rank rows and coarse rows of the sorted tables (built once per model)

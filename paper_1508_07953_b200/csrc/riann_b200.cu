@@ -169,6 +169,8 @@ struct PwTree {
 struct riann_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;  // heavy-query fallback, concurrent with the ring phases
+    cudaEvent_t ev_p0 = nullptr, ev_heavy = nullptr;
     int sms = 0;
     int smem_optin = 0;
     // model
@@ -186,7 +188,8 @@ struct riann_ctx {
     int ncoarse = 0;
     bool bulk_disabled = false;
     // bulk-path frame buffers
-    DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_counters, b_counts, b_starts, b_grouped, b_scan_tmp;
+    DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_grouped,
+        b_scan_tmp, overflow2;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -278,6 +281,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     RET(c->b_active[0].ensure((size_t)QN * 4));
     RET(c->b_active[1].ensure((size_t)QN * 4));
     RET(c->b_heavy.ensure((size_t)QN * 4));
+    RET(c->b_heavy2.ensure((size_t)QN * 4));
     RET(c->b_grouped.ensure((size_t)QN * 4));
     RET(c->b_counters.ensure(64));
     RET(c->b_counts.ensure((size_t)(n + 1) * 4));
@@ -286,7 +290,8 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, c->b_counts.as<int32_t>(), c->b_starts.as<int32_t>(),
                                      (int)(n + 1), c->stream));
     RET(c->b_scan_tmp.ensure(scan_bytes));
-    int32_t *ctr = c->b_counters.as<int32_t>();  // [0..1] active counts, [2] heavy, [3] item counter, [4..5] pool top
+    // [0..1] active counts, [2] P0 heavy, [3] item counter, [4..5] pool top, [6] ring heavy
+    int32_t *ctr = c->b_counters.as<int32_t>();
     CK(cudaMemsetAsync(ctr, 0, 64, c->stream));
 
     rb::BulkParams B;
@@ -332,7 +337,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     // P0
     {
         const int wpb = 8;
-        const size_t smem = (size_t)wpb * rb::K2_SMEM_BYTES;
+        const size_t smem = (size_t)wpb * 32 * (rb::p0_chunk_words(n) + 1) * 4;
         auto k = rb::bulk_p0_kernel<D>;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int bps = 0;
@@ -344,6 +349,28 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaGetLastError());
         c->launches += 1;
     }
+    // queries P0 could not take (first ring > LIGHT_MAX, pool full) run the
+    // per-query kernel on the second stream while the ring phases proceed
+    CK(cudaEventRecord(c->ev_p0, c->stream));
+    CK(cudaStreamWaitEvent(c->stream2, c->ev_p0, 0));
+    {
+        rb::QueryParams H = Pq;
+        H.qlist = B.heavy;
+        H.n_qlist = B.n_heavy;
+        cudaStream_t main = c->stream;
+        c->stream = c->stream2;
+        DevBuf keep = c->overflow;
+        c->overflow = c->overflow2;
+        const int r = c->idx16 ? launch_query_i<uint16_t>(c, H) : launch_query_i<int32_t>(c, H);
+        c->overflow2 = c->overflow;
+        c->overflow = keep;
+        c->stream = main;
+        RET(r);
+        c->launches += 1;
+    }
+    CK(cudaEventRecord(c->ev_heavy, c->stream2));
+    B.heavy = c->b_heavy2.as<int32_t>();
+    B.n_heavy = ctr + 6;
     // ring phases
     auto rk = rb::bulk_ring_kernel<D>;
     int ring_bps = 0;
@@ -402,9 +429,11 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaGetLastError());
         c->launches += 1;
     }
-    // heavy queries: the per-query kernel from scratch
+    // ring-phase stragglers (> BULK_U used anchors in S): per-query kernel from
+    // scratch on the main stream, then join the second stream
     Pq.qlist = B.heavy;
     Pq.n_qlist = B.n_heavy;
+    CK(cudaStreamWaitEvent(c->stream, c->ev_heavy, 0));
     return 1;
 }
 
@@ -746,6 +775,9 @@ int riann_ctx_create(int device, riann_ctx **out)
     c->sms = prop.multiProcessorCount;
     c->smem_optin = (int)prop.sharedMemPerBlockOptin;
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p0, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_heavy, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         delete c;
         return fail(RIANN_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
@@ -765,7 +797,7 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->pca_T, &c->refs_pca16, &c->e16p,
+                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
                       &c->units_pca, &c->e16max, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
@@ -777,6 +809,10 @@ int riann_ctx_destroy(riann_ctx *c)
         for (auto e : a) cudaEventDestroy(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->cublas) cublasDestroy(c->cublas);
+    cudaStreamSynchronize(c->stream2);
+    cudaEventDestroy(c->ev_p0);
+    cudaEventDestroy(c->ev_heavy);
+    cudaStreamDestroy(c->stream2);
     cudaStreamDestroy(c->stream);
     delete c;
     return 0;

@@ -199,26 +199,30 @@ __device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int cnt, uint3
 
 // ---------------------------------------------------------------------------
 // P0: first ring, candidate slot, first anchor.  One warp per query.
+// The first-ring window (unordered: distance order) becomes the ascending
+// candidate list (np.sort, search.py:116) through a per-warp n-bit bitmap in
+// shared memory; each lane owns a contiguous chunk of words, padded by one
+// word so the lanes' chunks fall in different banks.
+__host__ __device__ constexpr int p0_chunk_words(int64_t n) { return (int)(((n + 31) / 32 + 31) / 32); }
+
 template <int D>
 __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(16) uint32_t smem_w[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
-    unsigned char *ws = smem_raw + (size_t)wib * K2_SMEM_BYTES;
-    uint32_t *hist = reinterpret_cast<uint32_t *>(ws + 2 * LIST_BYTES);
-    const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const int64_t n = P.n;
+    const int CW = p0_chunk_words(n);  // words per lane chunk
+    const int stride = CW + 1;         // padded
+    uint32_t *bm = smem_w + (size_t)wib * 32 * stride;
+    const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const int64_t gwarp = (int64_t)blockIdx.x * wpb + wib;
-    uint16_t *spill = P.p0_spill + gwarp * 2 * LIGHT_MAX;
+    for (int i = lane; i < 32 * stride; i += 32) bm[i] = 0u;
+    __syncwarp();
     for (int64_t g = gwarp; g < P.Q; g += nwarps) {
-        QList<uint16_t> A{reinterpret_cast<uint16_t *>(ws), spill};
-        QList<uint16_t> B{reinterpret_cast<uint16_t *>(ws + LIST_BYTES), spill + LIGHT_MAX};
         const float *q = P.units + g * D;
         const int p = P.prev[g];
-        QState s;
-        s.status = ST_DONE;
         if (p < 0 || p >= n) {
             if (lane == 0) atomicExch(P.err, ERR_PREV_RANGE);
             if (lane == 0) P.st[g].status = ST_HEAVY + 100;  // skipped everywhere
@@ -242,56 +246,66 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             }
             continue;
         }
-        bool p_in = false;
+        // window of the u16 index row -> bitmap (16-byte vector loads on the aligned span)
         {
-            // window of the u16 index row: 16-byte vector loads over the aligned
-            // span, element-wise head and tail
             const uint16_t *row = P.sidx + (int64_t)p * n;
+            auto mark = [&](uint32_t j) {
+                const uint32_t w = j >> 5;
+                atomicOr(&bm[(w / CW) * stride + (w % CW)], 1u << (j & 31));
+            };
             const int64_t a0 = (lo + 7) & ~(int64_t)7, a1 = hi & ~(int64_t)7;
             if (a0 < a1) {
-                for (int64_t k = lo + lane; k < a0; k += 32) {
-                    const uint32_t j = __ldg(row + k);
-                    A.put((int)(k - lo), j);
-                    p_in |= (j == (uint32_t)p);
-                }
+                for (int64_t k = lo + lane; k < a0; k += 32) mark(__ldg(row + k));
                 for (int64_t v0 = a0 + (int64_t)lane * 8; v0 < a1; v0 += 256) {
                     const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + v0));
                     const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
 #pragma unroll
-                    for (int x = 0; x < 8; x++) {
-                        A.put((int)(v0 + x - lo), e8[x]);
-                        p_in |= (e8[x] == (uint16_t)p);
-                    }
+                    for (int x = 0; x < 8; x++) mark(e8[x]);
                 }
-                for (int64_t k = a1 + lane; k < hi; k += 32) {
-                    const uint32_t j = __ldg(row + k);
-                    A.put((int)(k - lo), j);
-                    p_in |= (j == (uint32_t)p);
-                }
+                for (int64_t k = a1 + lane; k < hi; k += 32) mark(__ldg(row + k));
             } else {
-                for (int64_t k = lo + lane; k < hi; k += 32) {
-                    const uint32_t j = __ldg(row + k);
-                    A.put((int)(k - lo), j);
-                    p_in |= (j == (uint32_t)p);
+                for (int64_t k = lo + lane; k < hi; k += 32) mark(__ldg(row + k));
+            }
+        }
+        __syncwarp();
+        // enumerate ascending into the slot; clear the bitmap
+        uint16_t *slot = P.pool + off;
+        const uint32_t *mine = bm + lane * stride;
+        int cnt = 0;
+        for (int w = 0; w < CW; w++) cnt += __popc(mine[w]);
+        const int inc = warp_incl_scan(cnt, lane);
+        int o = inc - cnt;
+        // rank of p among S (its position if present) and presence
+        const uint32_t wp = (uint32_t)p >> 5;
+        const int lp = (int)(wp / CW);
+        int below = 0;
+        bool p_in = false;
+        if (lane == lp) {
+            below = o;
+            for (int w = 0; w < (int)(wp % CW); w++) below += __popc(mine[w]);
+            const uint32_t word = mine[wp % CW];
+            below += __popc(word & ((1u << (p & 31)) - 1u));
+            p_in = (word >> (p & 31)) & 1u;
+        }
+        below = __shfl_sync(FULL, below, lp);
+        p_in = __shfl_sync(FULL, (int)p_in, lp);
+        for (int w = 0; w < CW; w++) {
+            uint32_t word = bm[lane * stride + w];
+            if (word) {
+                bm[lane * stride + w] = 0u;
+                const uint32_t base = (uint32_t)(lane * CW + w) * 32u;
+                while (word) {
+                    const int b = __ffs(word) - 1;
+                    word &= word - 1;
+                    slot[o++] = (uint16_t)(base + b);
                 }
             }
         }
-        p_in = __any_sync(FULL, p_in);
         __threadfence_block();
         __syncwarp();
-        const bool loop = cS >= P.L && P.max_rings > 1;
-        if (loop) warp_radix_sort(A, B, cS, P.passes, hist, lane);
-        uint16_t *slot = P.pool + off;  // 16-byte aligned (slots rounded to 8 entries)
-        {
-            const int cap = QList<uint16_t>::CAP;
-            const int nv = (min(cS, cap) + 7) / 8;
-            const uint4 *src = reinterpret_cast<const uint4 *>(A.sm);
-            uint4 *dst = reinterpret_cast<uint4 *>(slot);
-            for (int i = lane; i < nv; i += 32) dst[i] = src[i];
-            for (int i = cap + lane; i < cS; i += 32) slot[i] = (uint16_t)A.get(i);
-        }
-        __syncwarp();
         if (lane == 0) {
+            QState s;
+            const bool loop = cS >= P.L && P.max_rings > 1;
             s.d_prev = d;
             s.s_off = off;
             s.cS = cS;
@@ -304,10 +318,11 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             s.rng_has = 0;
             s.rng_buf = 0;
             s.sh = s.sl = s.ih = s.il = 0;
+            s.anchor = 0;
             int upos[BULK_U];
             if (p_in) {
                 s.u[0] = p;
-                upos[0] = lower_bound_u16(slot, cS, (uint32_t)p);
+                upos[0] = below;
                 s.nu = 1;
             }
             if (loop && cS - s.nu > 0) {
@@ -416,8 +431,10 @@ __global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
         icnt--;
         if (i >= m) break;
         const int64_t g = P.grouped[i];
-        QState s = P.st[g];
-        const int a = s.anchor;
+        QState *sp = P.st + g;
+        const int a = sp->anchor;
+        const int cS = sp->cS;
+        uint16_t *slot = P.pool + sp->s_off;
         const float *q = P.units + g * D;
         // search.py:131-133: exact d_a (numpy order), window on row a
         const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
@@ -425,71 +442,95 @@ __global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
         window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
                       __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
         const uint16_t *prow = P.pos + (int64_t)a * n;
-        // search.py:134: S' = S n ring, order kept, filtered in place
-        uint16_t *slot = P.pool + s.s_off;
-        const int cS = s.cS;
+        // search.py:134: S' = S n ring, order kept, filtered in place; per block of
+        // 1024 entries all list loads, then all rank lookups, are issued together
         int nh = 0;
-        for (int base = 0; base < cS; base += 256) {
-            const int i0 = base + lane * 8;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (i0 < cS) v = *reinterpret_cast<const uint4 *>(slot + i0);
-            const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
-            uint16_t pk[8];
+        for (int base = 0; base < cS; base += 1024) {
+            uint4 v[4];
 #pragma unroll
-            for (int x = 0; x < 8; x++) pk[x] = (i0 + x < cS) ? __ldg(prow + e8[x]) : (uint16_t)0xffff;
-            unsigned keepm = 0;
+            for (int k = 0; k < 4; k++) {
+                const int i0 = base + k * 256 + lane * 8;
+                v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
+            }
+            uint32_t keep4 = 0;  // 8 bits per k
 #pragma unroll
-            for (int x = 0; x < 8; x++)
-                if (i0 + x < cS && pk[x] >= lo && pk[x] < hi) keepm |= 1u << x;
-            const int kc = __popc(keepm);
-            const int inc = warp_incl_scan(kc, lane);
-            const int tot = __shfl_sync(FULL, inc, 31);
+            for (int k = 0; k < 4; k++) {
+                const int i0 = base + k * 256 + lane * 8;
+                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
+                uint16_t pk[8];
+#pragma unroll
+                for (int x = 0; x < 8; x++) pk[x] = (i0 + x < cS) ? __ldg(prow + e8[x]) : (uint16_t)0xffff;
+#pragma unroll
+                for (int x = 0; x < 8; x++)
+                    if (i0 + x < cS && pk[x] >= lo && pk[x] < hi) keep4 |= 1u << (8 * k + x);
+            }
             __syncwarp();
-            int o = nh + inc - kc;
 #pragma unroll
-            for (int x = 0; x < 8; x++)
-                if ((keepm >> x) & 1u) slot[o++] = e8[x];
-            nh += tot;
+            for (int k = 0; k < 4; k++) {
+                if (base + k * 256 >= cS) break;
+                const unsigned keepm = (keep4 >> (8 * k)) & 0xffu;
+                const int kc = __popc(keepm);
+                const int inc = warp_incl_scan(kc, lane);
+                const int tot = __shfl_sync(FULL, inc, 31);
+                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
+                int o = nh + inc - kc;
+#pragma unroll
+                for (int x = 0; x < 8; x++)
+                    if ((keepm >> x) & 1u) slot[o++] = e8[x];
+                nh += tot;
+            }
             __syncwarp();
         }
         if (lane == 0) {
-            s.tests += cS;
-            s.exact += 1;
-            s.rings += 1;
-            if (nh == 0) {
-                s.status = ST_DONE;  // search.py:136-137 rollback
-            } else {
-                s.cS = nh;
+            sp->tests += cS;
+            sp->exact += 1;
+            const int rings = sp->rings + 1;
+            sp->rings = rings;
+            int status = ST_DONE;  // nh == 0: search.py:136-137 rollback
+            if (nh > 0) {
+                sp->cS = nh;
+                int u[BULK_U];
                 int nu = 0;
-                for (int k = 0; k < s.nu; k++) {
-                    const int pk = __ldg(prow + s.u[k]);
-                    if (pk >= lo && pk < hi) s.u[nu++] = s.u[k];
+                const int nu0 = sp->nu;
+                for (int k = 0; k < nu0; k++) {
+                    const int uk = sp->u[k];
+                    const int pk = __ldg(prow + uk);
+                    if (pk >= lo && pk < hi) u[nu++] = uk;
                 }
-                s.nu = nu;
                 bool pin = false;
-                for (int k = 0; k < nu; k++) pin |= s.u[k] == P.prev[g];
-                s.p_in = pin;
-                s.status = ST_DONE;
-                if (nh >= P.L && s.rings < P.max_rings && nh - nu > 0) {
+                for (int k = 0; k < nu; k++) pin |= u[k] == P.prev[g];
+                sp->p_in = pin;
+                if (nh >= P.L && rings < P.max_rings && nh - nu > 0) {
                     int upos[BULK_U];
-                    for (int k = 0; k < nu; k++) upos[k] = lower_bound_u16(slot, nh, (uint32_t)s.u[k]);
+                    for (int k = 0; k < nu; k++) upos[k] = lower_bound_u16(slot, nh, (uint32_t)u[k]);
                     Pcg64 rng;
-                    rng_load(rng, s);
+                    rng.sh = sp->sh;
+                    rng.sl = sp->sl;
+                    rng.ih = sp->ih;
+                    rng.il = sp->il;
+                    rng.has = sp->rng_has;
+                    rng.buf = sp->rng_buf;
                     const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
                     const int pos = avail_pos(k, upos, nu);
                     if (nu >= BULK_U) {
-                        s.status = ST_HEAVY;
+                        status = ST_HEAVY;
                         P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
                     } else {
-                        s.anchor = (int)slot[pos];
-                        s.u[s.nu++] = s.anchor;
-                        rng_store(s, rng);
-                        s.status = ST_ACTIVE;
+                        const int an = (int)slot[pos];
+                        sp->anchor = an;
+                        u[nu++] = an;
+                        sp->sh = rng.sh;
+                        sp->sl = rng.sl;
+                        sp->rng_has = rng.has;
+                        sp->rng_buf = rng.buf;
+                        status = ST_ACTIVE;
                         P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
                     }
                 }
+                for (int k = 0; k < nu; k++) sp->u[k] = u[k];
+                sp->nu = nu;
             }
-            P.st[g] = s;
+            sp->status = status;
         }
         __syncwarp();
     }

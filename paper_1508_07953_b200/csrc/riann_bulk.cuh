@@ -25,7 +25,7 @@ namespace rb {
 
 constexpr int LIGHT_MAX = 16384;  // largest first ring handled by the bulk path (u16 entries)
 constexpr int BULK_U = 4;        // used anchors tracked per query
-constexpr int COARSE = 256;      // coarse index stride of the sorted rows
+constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 constexpr int PH_WARPS = 16;     // warps per ring-phase CTA
 constexpr int PH_CHUNK = 64;     // queries per ring-phase work item
 
@@ -119,67 +119,57 @@ __device__ __forceinline__ void rng_store(QState &s, const Pcg64 &r)
     s.rng_buf = r.buf;
 }
 
-// searchsorted pair on a sorted row through its coarse index (every COARSE-th
-// value): lo = first v >= lv, hi = first v > hv.  The whole coarse row and the
-// two <= COARSE-entry fine segments are read with independent vector loads (two
-// round trips); counts of predicate-true entries are the positions because the
-// rows are sorted.
-__device__ __forceinline__ void window_coarse(const float *__restrict__ row, const float *__restrict__ cs, int nb,
-                                              int64_t n, double lv, double hv, int lane, int64_t &lo, int64_t &hi)
+// searchsorted pair on a sorted row through its coarse index: returns
+// lo = first v >= lv and hi = first v > hv.  The coarse array (shared or global
+// memory) is searched 17-ary by the two half-warps (as ring_window); the
+// remaining <= 65 entries of the row are counted.
+__device__ __forceinline__ void window_coarse(const float *__restrict__ row, const float *cs, int nb, int64_t n,
+                                              double lv, double hv, int lane, int64_t &lo, int64_t &hi)
 {
-    int clt = 0, cle = 0;
-    for (int i0 = 0; i0 < nb; i0 += 256) {
-        float v[8];
-#pragma unroll
-        for (int x = 0; x < 8; x++) {
-            const int i = i0 + x * 32 + lane;
-            v[x] = i < nb ? __ldg(cs + i) : __int_as_float(0x7f800000);
+    const int h = lane >> 4, hl = lane & 15;
+    const double thr = h ? hv : lv;
+    int b0 = 0, b1 = nb;  // first coarse entry failing the predicate lies in [b0, b1]
+    for (;;) {
+        const int s = b1 - b0;
+        if (!__any_sync(FULL, s > 16)) break;
+        const int p = b0 + (int)(((int64_t)(hl + 1) * s) / 17);
+        bool pr = false;
+        if (s > 16) {
+            const double v = (double)cs[p];
+            pr = h ? (v <= thr) : (v < thr);
         }
-#pragma unroll
-        for (int x = 0; x < 8; x++) {
-            const double dv = (double)v[x];
-            clt += dv < lv ? 1 : 0;
-            cle += dv <= hv ? 1 : 0;
+        const unsigned ball = __ballot_sync(FULL, pr);
+        const int c = __popc((ball >> (h * 16)) & 0xffffu);
+        const int p_lo = __shfl_sync(FULL, p, h * 16 + (c > 0 ? c - 1 : 0));
+        const int p_hi = __shfl_sync(FULL, p, h * 16 + (c < 16 ? c : 15));
+        if (s > 16) {
+            if (c > 0) b0 = p_lo + 1;
+            if (c < 16) b1 = p_hi;
         }
     }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        clt += __shfl_xor_sync(FULL, clt, o);
-        cle += __shfl_xor_sync(FULL, cle, o);
+    {
+        const int p = b0 + hl;
+        bool pr = false;
+        if (p < b1) {
+            const double v = (double)cs[p];
+            pr = h ? (v <= thr) : (v < thr);
+        }
+        const unsigned ball = __ballot_sync(FULL, pr);
+        b0 += __popc((ball >> (h * 16)) & 0xffffu);
     }
-    // coarse entries [0, b) satisfy the predicate; the answer lies in
-    // (COARSE*(b-1), COARSE*b] (or is 0 / n at the ends)
-    auto seg = [&](int b, int64_t &s0, int64_t &s1) {
-        s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
-        s1 = (b < nb) ? (int64_t)b * COARSE : n;
-    };
-    int64_t a0, a1, b0, b1;
-    seg(clt, a0, a1);
-    seg(cle, b0, b1);
-    float va[8], vb[8];
-#pragma unroll
-    for (int x = 0; x < 8; x++) {
-        const int64_t ka = a0 + x * 32 + lane, kb = b0 + x * 32 + lane;
-        va[x] = ka < a1 ? __ldg(row + ka) : __int_as_float(0x7f800000);
-        vb[x] = kb < b1 ? __ldg(row + kb) : __int_as_float(0x7f800000);
+    const int b = b0;  // coarse entries [0, b) satisfy the predicate
+    const int64_t s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
+    const int64_t s1 = (b < nb) ? (int64_t)b * COARSE : n;
+    int cnt = 0;
+    for (int64_t k = s0 + hl; k < s1; k += 16) {
+        const double v = (double)__ldg(row + k);
+        cnt += (h ? (v <= thr) : (v < thr)) ? 1 : 0;
     }
-    int fa = 0, fb = 0;
 #pragma unroll
-    for (int x = 0; x < 8; x++) {
-        fa += (double)va[x] < lv ? 1 : 0;
-        fb += (double)vb[x] <= hv ? 1 : 0;
-    }
-    // segments longer than 256 entries only occur for n-COARSE*(nb-1) > 256: not
-    // with COARSE = 256, but keep exactness for any shape
-    for (int64_t k = a0 + 256 + lane; k < a1; k += 32) fa += (double)__ldg(row + k) < lv ? 1 : 0;
-    for (int64_t k = b0 + 256 + lane; k < b1; k += 32) fb += (double)__ldg(row + k) <= hv ? 1 : 0;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        fa += __shfl_xor_sync(FULL, fa, o);
-        fb += __shfl_xor_sync(FULL, fb, o);
-    }
-    lo = a0 + fa;
-    hi = b0 + fb;
+    for (int o = 1; o < 16; o <<= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    const int64_t res = s0 + cnt;
+    lo = __shfl_sync(FULL, res, 0);
+    hi = __shfl_sync(FULL, res, 16);
 }
 
 // k-th (0-based) element of ascending list S minus the used anchors u[0..nu)

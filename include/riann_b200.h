@@ -118,6 +118,10 @@ int riann_set_prev_units(riann_ctx *ctx, const float *units, int64_t rows, int d
  * of frames and of kernel launches since enable. */
 int riann_timing_enable(riann_ctx *ctx, int on);
 int riann_timing_read(riann_ctx *ctx, double *ms3, uint64_t *frames, uint64_t *launches);
+/* Snapshot / restore of the device-resident stream state (previous field and
+ * previous units), e.g. to replay the same frames; one snapshot per context. */
+int riann_state_save(riann_ctx *ctx);
+int riann_state_restore(riann_ctx *ctx);
 /* Read back the device-resident field of the last frame. */
 int riann_field_get(riann_ctx *ctx, int32_t *idx, double *dist, int64_t count);
 

@@ -58,6 +58,8 @@ SIGNATURES = {
                                   P, P, C.POINTER(FrameStatsC)]),
     "riann_set_prev_units": (i32, [P, P, i64, i32]),
     "riann_field_get": (i32, [P, P, P, i64]),
+    "riann_state_save": (i32, [P]),
+    "riann_state_restore": (i32, [P]),
     "riann_timing_enable": (i32, [P, i32]),
     "riann_timing_read": (i32, [P, P, C.POINTER(u64), C.POINTER(u64)]),
     "riann_frame_units": (i32, [P, P, i32, i32, i32, P, P]),

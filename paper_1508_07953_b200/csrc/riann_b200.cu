@@ -199,6 +199,10 @@ struct riann_ctx {
     int cur_fld = 0;
     int64_t field_count = -1;
     PwTree tree;
+    // state snapshot (riann_state_save / riann_state_restore)
+    DevBuf snap_idx, snap_units;
+    int64_t snap_field = -1, snap_units_rows = 0;
+    bool snap_have_units = false, snap_valid = false;
     // per-kernel event timing of the frame path (riann_timing_*)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -798,7 +802,7 @@ int riann_ctx_destroy(riann_ctx *c)
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
                       &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
-                      &c->units_pca, &c->e16max, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
+                      &c->units_pca, &c->e16max, &c->snap_idx, &c->snap_units, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
                       &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,
@@ -1213,6 +1217,47 @@ int riann_timing_read(riann_ctx *c, double *ms3, uint64_t *frames, uint64_t *lau
         for (int k = 0; k < 3; k++) ms3[k] = c->t_ms[k];
     if (frames) *frames = c->t_frames;
     if (launches) *launches = c->launches;
+    return 0;
+}
+
+int riann_state_save(riann_ctx *c)
+{
+    RET(check_model(c, true));
+    if (c->field_count < 0) return fail(RIANN_E_STATE, "no device-resident field to save");
+    RET(c->use());
+    const int64_t Q = c->field_count;
+    RET(c->snap_idx.ensure((size_t)Q * 4));
+    CK(cudaMemcpyAsync(c->snap_idx.p, c->fld_idx[c->cur_fld].p, (size_t)Q * 4, cudaMemcpyDeviceToDevice, c->stream));
+    c->snap_have_units = c->have_prev_units;
+    c->snap_units_rows = c->prev_units_rows;
+    if (c->have_prev_units) {
+        const size_t ub = (size_t)c->prev_units_rows * c->dim * 4;
+        RET(c->snap_units.ensure(ub));
+        CK(cudaMemcpyAsync(c->snap_units.p, c->units[c->cur_units ^ 1].p, ub, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->snap_field = Q;
+    c->snap_valid = true;
+    return 0;
+}
+
+int riann_state_restore(riann_ctx *c)
+{
+    RET(check_model(c, true));
+    if (!c->snap_valid) return fail(RIANN_E_STATE, "no saved state");
+    RET(c->use());
+    const int64_t Q = c->snap_field;
+    RET(c->fld_idx[c->cur_fld].ensure((size_t)Q * 4));
+    CK(cudaMemcpyAsync(c->fld_idx[c->cur_fld].p, c->snap_idx.p, (size_t)Q * 4, cudaMemcpyDeviceToDevice, c->stream));
+    c->field_count = Q;
+    c->have_prev_units = c->snap_have_units;
+    c->prev_units_rows = c->snap_units_rows;
+    if (c->snap_have_units) {
+        const size_t ub = (size_t)c->snap_units_rows * c->dim * 4;
+        RET(c->units[c->cur_units ^ 1].ensure(ub));
+        CK(cudaMemcpyAsync(c->units[c->cur_units ^ 1].p, c->snap_units.p, ub, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
 

@@ -561,7 +561,7 @@ struct ScreenParams {
 constexpr int FB = 512;  // candidates per screening block
 
 template <int D>
-__global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P, ScreenParams SP)
+__global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, ScreenParams SP)
 {
     constexpr int GX = Lay<D>::G;
     constexpr int NGX = WARP / GX;
@@ -640,62 +640,35 @@ __global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P, Screen
                 }
             }
             int nA = 0;
-            // candidate indices of the block, 16 per lane (lane l: entries
-            // 16l..16l+15; order is irrelevant to the argmin)
-            uint32_t jp[8];  // packed pairs of u16 indices
-            {
-                const int e = lane * 16;
-                if (e + 16 <= bn) {
-                    const uint4 *src = reinterpret_cast<const uint4 *>(slot + blk + e);
-                    const uint4 a = src[0], b = src[1];
-                    jp[0] = a.x; jp[1] = a.y; jp[2] = a.z; jp[3] = a.w;
-                    jp[4] = b.x; jp[5] = b.y; jp[6] = b.z; jp[7] = b.w;
-                } else {
-#pragma unroll
-                    for (int x = 0; x < 8; x++) {
-                        const uint32_t lo16 = e + 2 * x < bn ? slot[blk + e + 2 * x] : slot[blk];
-                        const uint32_t hi16 = e + 2 * x + 1 < bn ? slot[blk + e + 2 * x + 1] : slot[blk];
-                        jp[x] = lo16 | (hi16 << 16);
-                    }
-                }
-            }
-            auto jr_at = [&](int x) -> uint32_t { return (jp[x >> 1] >> ((x & 1) * 16)) & 0xffffu; };
-#pragma unroll
-            for (int u0 = 0; u0 < 16; u0 += 4) {
-                if (!__any_sync(FULL, lane * 16 + u0 < bn)) break;
-                uint4 v0[4], v1[4];
+            for (int e0 = 0; e0 < bn; e0 += 32) {
+                const int e = e0 + lane;
+                const bool valid = e < bn;
+                const uint32_t j = slot[blk + (valid ? e : 0)];
+                const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D);
+                const uint4 v0 = ld_keep16(rp, pol_keep), v1 = ld_keep16(rp + 1, pol_keep);
+                float s = 0.f;
+                const __half2 *h0 = reinterpret_cast<const __half2 *>(&v0);
+                const __half2 *h1 = reinterpret_cast<const __half2 *>(&v1);
 #pragma unroll
                 for (int x = 0; x < 4; x++) {
-                    const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)jr_at(u0 + x) * D);
-                    v0[x] = ld_keep16(rp, pol_keep);
-                    v1[x] = ld_keep16(rp + 1, pol_keep);
+                    float2 f = __half22float2(h0[x]);
+                    float a0 = __fsub_rn(f.x, qc[2 * x]), a1 = __fsub_rn(f.y, qc[2 * x + 1]);
+                    s = __fmaf_rn(a0, a0, s);
+                    s = __fmaf_rn(a1, a1, s);
+                    f = __half22float2(h1[x]);
+                    a0 = __fsub_rn(f.x, qc[8 + 2 * x]);
+                    a1 = __fsub_rn(f.y, qc[8 + 2 * x + 1]);
+                    s = __fmaf_rn(a0, a0, s);
+                    s = __fmaf_rn(a1, a1, s);
                 }
-#pragma unroll
-                for (int x = 0; x < 4; x++) {
-                    float s = 0.f;
-                    const __half2 *h0 = reinterpret_cast<const __half2 *>(&v0[x]);
-                    const __half2 *h1 = reinterpret_cast<const __half2 *>(&v1[x]);
-#pragma unroll
-                    for (int y = 0; y < 4; y++) {
-                        float2 f = __half22float2(h0[y]);
-                        float a0 = __fsub_rn(f.x, qc[2 * y]), a1 = __fsub_rn(f.y, qc[2 * y + 1]);
-                        s = __fmaf_rn(a0, a0, s);
-                        s = __fmaf_rn(a1, a1, s);
-                        f = __half22float2(h1[y]);
-                        a0 = __fsub_rn(f.x, qc[8 + 2 * y]);
-                        a1 = __fsub_rn(f.y, qc[8 + 2 * y + 1]);
-                        s = __fmaf_rn(a0, a0, s);
-                        s = __fmaf_rn(a1, a1, s);
-                    }
-                    const bool keep = lane * 16 + u0 + x < bn && lb_of(s, SP.slack) <= ub;
-                    const unsigned ball = __ballot_sync(FULL, keep);
-                    if (keep) {
-                        const int o = nA + __popc(ball & lanemask_lt());
-                        Aj[o] = jr_at(u0 + x);
-                        As[o] = s;
-                    }
-                    nA += __popc(ball);
+                const bool keep = valid && lb_of(s, SP.slack) <= ub;
+                const unsigned ball = __ballot_sync(FULL, keep);
+                if (keep) {
+                    const int o = nA + __popc(ball & lanemask_lt());
+                    Aj[o] = j;
+                    As[o] = s;
                 }
+                nA += __popc(ball);
             }
             __syncwarp();
             // further chunks for the candidates still alive
@@ -720,7 +693,6 @@ __global__ void __launch_bounds__(256, 2) bulk_final_kernel(BulkParams P, Screen
                     float s = valid ? As[i] : 0.f;
                     const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D) + 2 * c;
                     const uint4 v0 = ld_keep16(rp, pol_keep), v1 = ld_keep16(rp + 1, pol_keep);
-                    // (one candidate per lane: survivors of chunk 0 are few)
                     const __half2 *h0 = reinterpret_cast<const __half2 *>(&v0);
                     const __half2 *h1 = reinterpret_cast<const __half2 *>(&v1);
 #pragma unroll

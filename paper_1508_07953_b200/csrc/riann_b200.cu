@@ -189,7 +189,7 @@ struct riann_ctx {
     bool bulk_disabled = false;
     // bulk-path frame buffers
     DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_grouped,
-        b_scan_tmp, overflow2;
+        b_scan_tmp, overflow2, b_item_counts, b_item_starts, b_items;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -290,6 +290,9 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     RET(c->b_counters.ensure(64));
     RET(c->b_counts.ensure((size_t)(n + 1) * 4));
     RET(c->b_starts.ensure((size_t)(n + 1) * 4));
+    RET(c->b_item_counts.ensure((size_t)(n + 1) * 4));
+    RET(c->b_item_starts.ensure((size_t)(n + 1) * 4));
+    RET(c->b_items.ensure((size_t)(QN + n + 1) * 16));
     size_t scan_bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, c->b_counts.as<int32_t>(), c->b_starts.as<int32_t>(),
                                      (int)(n + 1), c->stream));
@@ -333,6 +336,9 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.starts = c->b_starts.as<int32_t>();
     B.grouped = c->b_grouped.as<int32_t>();
     B.item_next = ctr + 3;
+    B.item_counts = c->b_item_counts.as<int32_t>();
+    B.item_starts = c->b_item_starts.as<int32_t>();
+    B.items = c->b_items.as<int4>();
     B.out_idx = Pq.out_idx;
     B.out_dist = Pq.out_dist;
     B.stats = Pq.stats;
@@ -375,11 +381,15 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cudaEventRecord(c->ev_heavy, c->stream2));
     B.heavy = c->b_heavy2.as<int32_t>();
     B.n_heavy = ctr + 6;
-    // ring phases
+    // ring phases: windows (warp per query) -> counting sort by anchor ->
+    // work items -> TMA-staged rank rows (CTA per SM)
+    auto wk = rb::bulk_window_kernel<D>;
+    int win_bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&win_bps, wk, 256, 0));
+    const unsigned win_grid = (unsigned)(c->sms * std::max(win_bps, 1));
     auto rk = rb::bulk_ring_kernel<D>;
-    int ring_bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ring_bps, rk, 256, 0));
-    const unsigned ring_grid = (unsigned)(c->sms * std::max(ring_bps, 1));
+    const size_t ring_smem = (size_t)3 * n;
+    CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem));
     const unsigned small_grid = (unsigned)c->sms * 4;
     const int phases = Pq.max_rings - 1;
     for (int ph = 0; ph < phases; ph++) {
@@ -395,17 +405,25 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
             if (h == 0) break;
         }
         CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
-        CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
+        CK(cudaMemsetAsync(B.item_counts + n, 0, 4, c->stream));
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
+        wk<<<win_grid, 256, 0, c->stream>>>(B);
+        CK(cudaGetLastError());
         rb::bulk_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
         CK(cub::DeviceScan::ExclusiveSum(c->b_scan_tmp.p, scan_bytes, B.counts, B.starts, (int)(n + 1), c->stream));
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
-        rk<<<ring_grid, 256, 0, c->stream>>>(B);
+        rb::bulk_item_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
-        c->launches += 3;
+        CK(cub::DeviceScan::ExclusiveSum(c->b_scan_tmp.p, scan_bytes, B.item_counts, B.item_starts, (int)(n + 1),
+                                         c->stream));
+        rb::bulk_item_fill_kernel<<<small_grid, 256, 0, c->stream>>>(B);
+        CK(cudaGetLastError());
+        rk<<<(unsigned)c->sms, rb::RING_WARPS * 32, ring_smem, c->stream>>>(B);
+        CK(cudaGetLastError());
+        c->launches += 6;
     }
     // final scan of the light queries (PCA-basis screening)
     {
@@ -450,7 +468,7 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
     P.passes = (bits + 7) / 8;
     if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && c->pca && !c->bulk_disabled &&
-        (c->dim == 64 || c->dim == 192) && c->n % 8 == 0) {
+        (c->dim == 64 || c->dim == 192) && c->n % 16 == 0 && 3 * c->n <= c->smem_optin) {
         int r = c->dim == 64 ? run_bulk_t<64>(c, P) : run_bulk_t<192>(c, P);
         if (r != 1) return r;
         // falls through: P.qlist = heavy queries
@@ -801,7 +819,8 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
+                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->b_heavy2, &c->overflow2,
+                      &c->b_item_counts, &c->b_item_starts, &c->b_items, &c->pca_T, &c->refs_pca16, &c->e16p,
                       &c->units_pca, &c->e16max, &c->snap_idx, &c->snap_units, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,

@@ -381,49 +381,54 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cudaEventRecord(c->ev_heavy, c->stream2));
     B.heavy = c->b_heavy2.as<int32_t>();
     B.n_heavy = ctr + 6;
-    // ring phases: windows (warp per query) -> counting sort by anchor ->
-    // work items -> TMA-staged rank rows (CTA per SM)
+    // ring phases: window/draw pass (warp per query) -> counting sort by
+    // anchor -> filter pass in anchor order; a last window pass applies the
+    // final intersection
     auto wk = rb::bulk_window_kernel<D>;
     int win_bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&win_bps, wk, 256, 0));
     const unsigned win_grid = (unsigned)(c->sms * std::max(win_bps, 1));
-    auto rk = rb::bulk_ring_kernel<D>;
-    const size_t ring_smem = (size_t)3 * n;
-    CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem));
+    auto rk = rb::bulk_ring_kernel;
+    int ring_bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ring_bps, rk, 256, 0));
+    const unsigned ring_grid = (unsigned)(c->sms * std::max(ring_bps, 1));
     const unsigned small_grid = (unsigned)c->sms * 4;
     const int phases = Pq.max_rings - 1;
-    for (int ph = 0; ph < phases; ph++) {
-        const int in = ph & 1, out = in ^ 1;
-        B.active_in = c->b_active[in].as<int32_t>();
-        B.n_active_in = ctr + in;
-        B.active_out = c->b_active[out].as<int32_t>();
-        B.n_active_out = ctr + out;
-        if (ph >= 15) {  // long ring caps: stop once no query is left
+    // lists: P0 wrote its queries (first anchor drawn) to active[0]
+    int cur = 0;  // list holding the queries to process next
+    for (int ph = 0; ph <= phases; ph++) {
+        const int nxt = cur ^ 1;
+        const bool last = ph == phases;
+        if (ph >= 16 && !last) {  // long ring caps: stop once no query is left
             int32_t h = 0;
-            CK(cudaMemcpyAsync(&h, ctr + in, 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(&h, ctr + cur, 4, cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
             if (h == 0) break;
         }
-        CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
-        CK(cudaMemsetAsync(B.item_counts + n, 0, 4, c->stream));
-        CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
-        wk<<<win_grid, 256, 0, c->stream>>>(B);
+        B.active_in = c->b_active[cur].as<int32_t>();
+        B.n_active_in = ctr + cur;
+        B.active_out = c->b_active[nxt].as<int32_t>();
+        B.n_active_out = ctr + nxt;
+        CK(cudaMemsetAsync(ctr + nxt, 0, 4, c->stream));
+        wk<<<win_grid, 256, 0, c->stream>>>(B, last ? 1 : 0);
         CK(cudaGetLastError());
+        c->launches += 1;
+        if (last) break;
+        // filter the queries that drew an anchor (list nxt), grouped by anchor
+        B.active_in = c->b_active[nxt].as<int32_t>();
+        B.n_active_in = ctr + nxt;
+        CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
+        CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
         CK(cub::DeviceScan::ExclusiveSum(c->b_scan_tmp.p, scan_bytes, B.counts, B.starts, (int)(n + 1), c->stream));
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
-        rb::bulk_item_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
+        rk<<<ring_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
-        CK(cub::DeviceScan::ExclusiveSum(c->b_scan_tmp.p, scan_bytes, B.item_counts, B.item_starts, (int)(n + 1),
-                                         c->stream));
-        rb::bulk_item_fill_kernel<<<small_grid, 256, 0, c->stream>>>(B);
-        CK(cudaGetLastError());
-        rk<<<(unsigned)c->sms, rb::RING_WARPS * 32, ring_smem, c->stream>>>(B);
-        CK(cudaGetLastError());
-        c->launches += 6;
+        c->launches += 3;
+        cur = nxt;
     }
     // final scan of the light queries (PCA-basis screening)
     {
@@ -468,7 +473,7 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
     P.passes = (bits + 7) / 8;
     if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && c->pca && !c->bulk_disabled &&
-        (c->dim == 64 || c->dim == 192) && c->n % 16 == 0 && 3 * c->n <= c->smem_optin) {
+        (c->dim == 64 || c->dim == 192) && c->n % 8 == 0) {
         int r = c->dim == 64 ? run_bulk_t<64>(c, P) : run_bulk_t<192>(c, P);
         if (r != 1) return r;
         // falls through: P.qlist = heavy queries

@@ -29,7 +29,7 @@ constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 constexpr int PH_WARPS = 16;     // warps per ring-phase CTA
 constexpr int PH_CHUNK = 64;     // queries per ring-phase work item
 
-enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
+enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2, ST_FILTERED = 3 };
 
 struct __align__(16) QState {
     double d_prev;
@@ -39,7 +39,7 @@ struct __align__(16) QState {
     int32_t anchor, nu, rng_has, p_in;
     uint32_t rng_buf;
     int32_t tests, exact, wlo;  // [wlo, whi): the current anchor's window
-    int32_t whi, ukeep, pad0, pad1;  // ukeep: used anchors that stay in the ring (bit mask)
+    int32_t whi, ukeep, fres, pad1;  // ukeep: used anchors in the ring (mask); fres: |S n ring|
     int32_t u[BULK_U];
 };
 
@@ -410,11 +410,14 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigne
 }
 
 // ---------------------------------------------------------------------------
-// Ring phase, part 1 (warp per active query): exact d_a of the drawn anchor
-// (search.py:131, numpy order), its window [wlo, whi) on the anchor's sorted
-// row (search.py:133 via :77-79), and which used anchors stay in the ring.
+// Ring phase, part 1 ("window"): warp per query of the previous phase's list.
+// Applies the previous intersection (search.py:134-138: rings += 1, rollback
+// on empty, S = S'), tests the loop condition (search.py:121), draws the next
+// anchor (search.py:122-130, numpy RNG) and computes its exact distance
+// (numpy order) and window [wlo, whi) on the anchor's sorted row.  Queries
+// that continue go to active_out.  apply_only: the ring cap is reached.
 template <int D>
-__global__ void __launch_bounds__(256) bulk_window_kernel(BulkParams P)
+__global__ void __launch_bounds__(256) bulk_window_kernel(BulkParams P, int apply_only)
 {
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -424,7 +427,64 @@ __global__ void __launch_bounds__(256) bulk_window_kernel(BulkParams P)
     for (int64_t i = gwarp; i < m; i += nwarps) {
         const int64_t g = P.active_in[i];
         QState *sp = P.st + g;
-        const int a = sp->anchor;
+        int go = 1, a = 0;
+        if (lane == 0) {
+            a = sp->anchor;
+            if (sp->status == ST_FILTERED) {
+                const int cS = sp->cS, nh = sp->fres;
+                sp->tests += cS;
+                sp->exact += 1;
+                const int rings = sp->rings + 1;
+                sp->rings = rings;
+                go = 0;
+                int status = ST_DONE;  // nh == 0: rollback, keep S
+                if (nh > 0) {
+                    sp->cS = nh;
+                    const uint16_t *slot = P.pool + sp->s_off;
+                    int uu[BULK_U];
+                    int nu = 0;
+                    const int nu0 = sp->nu, km = sp->ukeep;
+                    for (int q2 = 0; q2 < nu0; q2++)
+                        if ((km >> q2) & 1) uu[nu++] = sp->u[q2];
+                    bool pin = false;
+                    for (int q2 = 0; q2 < nu; q2++) pin |= uu[q2] == P.prev[g];
+                    sp->p_in = pin;
+                    if (!apply_only && nh >= P.L && rings < P.max_rings && nh - nu > 0) {
+                        int upos[BULK_U];
+                        for (int q2 = 0; q2 < nu; q2++) upos[q2] = lower_bound_u16(slot, nh, (uint32_t)uu[q2]);
+                        Pcg64 rng;
+                        rng.sh = sp->sh;
+                        rng.sl = sp->sl;
+                        rng.ih = sp->ih;
+                        rng.il = sp->il;
+                        rng.has = sp->rng_has;
+                        rng.buf = sp->rng_buf;
+                        const int kk = (int)pcg_integers(rng, (uint64_t)(nh - nu));
+                        const int pos = avail_pos(kk, upos, nu);
+                        if (nu >= BULK_U) {
+                            status = ST_HEAVY;
+                            P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
+                        } else {
+                            a = (int)slot[pos];
+                            sp->anchor = a;
+                            uu[nu++] = a;
+                            sp->sh = rng.sh;
+                            sp->sl = rng.sl;
+                            sp->rng_has = rng.has;
+                            sp->rng_buf = rng.buf;
+                            status = ST_ACTIVE;
+                            go = 1;
+                        }
+                    }
+                    for (int q2 = 0; q2 < nu; q2++) sp->u[q2] = uu[q2];
+                    sp->nu = nu;
+                }
+                sp->status = status;
+            }
+        }
+        go = __shfl_sync(FULL, go, 0);
+        if (!go) continue;
+        a = __shfl_sync(FULL, a, 0);
         const float *q = P.units + g * D;
         const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
         int64_t lo, hi;
@@ -441,194 +501,81 @@ __global__ void __launch_bounds__(256) bulk_window_kernel(BulkParams P)
             sp->wlo = (int32_t)lo;
             sp->whi = (int32_t)hi;
             sp->ukeep = (int32_t)km;
+            P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
         }
     }
 }
 
-// work items: each anchor's group of queries in chunks of PH_CHUNK
-__global__ void bulk_item_count_kernel(BulkParams P)
+// ---------------------------------------------------------------------------
+// Ring phase, part 2 ("filter"): one warp per query, queries in anchor order
+// with dynamic chunked scheduling so the ~200 anchor rank rows in flight stay
+// L2-resident.  S' = S n ring (search.py:134): lo <= pos[a][j] < hi for every
+// candidate, 8-deep independent lookups per lane, in-place order-preserving
+// compaction.  The result is applied by the next window pass.
+__global__ void __launch_bounds__(256) bulk_ring_kernel(BulkParams P)
 {
-    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < P.n; a += (int64_t)gridDim.x * blockDim.x)
-        P.item_counts[a] = (P.counts[a] + PH_CHUNK - 1) / PH_CHUNK;
-}
-
-__global__ void bulk_item_fill_kernel(BulkParams P)
-{
-    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < P.n; a += (int64_t)gridDim.x * blockDim.x) {
-        const int c = P.counts[a];
-        const int s0 = P.starts[a], i0 = P.item_starts[a];
-        for (int k = 0; k * PH_CHUNK < c; k++)
-            P.items[i0 + k] = make_int4((int)a, s0 + k * PH_CHUNK, min(PH_CHUNK, c - k * PH_CHUNK), 0);
-    }
-}
-
-// Ring phase, part 2: one CTA (32 warps) per SM walks its work items; each
-// item's anchor rank row pos[a][*] arrives in two half-row TMA bulk copies
-// (n bytes each) through a 3-slot shared-memory ring, so the copies of the
-// next half-rows overlap the filtering of the current one.  Candidates are
-// filtered in place, order kept (search.py:134), half by half (S is sorted,
-// so the first half of the columns is a prefix of S).
-constexpr int RING_WARPS = 32;
-
-template <int D>
-__global__ void __launch_bounds__(RING_WARPS * 32, 1) bulk_ring_kernel(BulkParams P)
-{
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ uint64_t bars[3];
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
     const int64_t n = P.n;
-    const int64_t half = n / 2;
-    uint16_t *slots[3] = {reinterpret_cast<uint16_t *>(smem_raw), reinterpret_cast<uint16_t *>(smem_raw + n),
-                          reinterpret_cast<uint16_t *>(smem_raw + 2 * n)};
-    const int T = P.item_starts[n];
-    const int G = gridDim.x;
-    auto item_of = [&](int k) { return (int)blockIdx.x + (k >> 1) * G; };
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < 3; i++) mbar_init(&bars[i], 1);
-    }
-    __syncthreads();
-    auto issue = [&](int k) {  // thread 0 only
-        const int it = item_of(k);
-        if (it >= T) return;
-        const int a = P.items[it].x;
-        const int sl = k % 3;
-        mbar_expect_tx(&bars[sl], (unsigned)n);
-        tma_bulk_g2s(slots[sl], P.pos + (int64_t)a * n + (k & 1) * half, (unsigned)n, &bars[sl]);
-    };
-    if (threadIdx.x == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(0);
-        issue(1);
-        issue(2);
-    }
-    // per-warp carry between the two halves (up to 2 queries per warp per item)
-    int carry_m[2] = {0, 0}, carry_nh[2] = {0, 0};
-    for (int k = 0;; k++) {
-        const int it = item_of(k);
-        if (it >= T) break;
-        const int h = k & 1;
-        const int4 item = P.items[it];
-        const int a = item.x;
-        mbar_wait(&bars[k % 3], (unsigned)((k / 3) & 1));
-        const uint16_t *prow = slots[k % 3];
-        const uint32_t jlo = (uint32_t)(h * half), jhi = (uint32_t)(h ? n : half);
+    const int m = *P.n_active_in;
+    constexpr int GRAB = 4;
+    int ibase = 0, icnt = 0;
+    for (;;) {
+        if (icnt == 0) {
+            int b = 0;
+            if (lane == 0) b = atomicAdd(P.item_next, GRAB);
+            ibase = __shfl_sync(FULL, b, 0);
+            icnt = GRAB;
+        }
+        const int i = ibase + (GRAB - icnt);
+        icnt--;
+        if (i >= m) break;
+        const int64_t g = P.grouped[i];
+        QState *sp = P.st + g;
+        const int a = sp->anchor;
+        const int cS = sp->cS;
+        const int lo = sp->wlo, hi = sp->whi;
+        uint16_t *slot = P.pool + sp->s_off;
+        const uint16_t *prow = P.pos + (int64_t)a * n;
+        int nh = 0;
+        for (int base = 0; base < cS; base += 1024) {
+            uint4 v[4];
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
-            const int e = w + u * RING_WARPS;
-            if (e >= item.z) continue;
-            const int64_t g = P.grouped[item.y + e];
-            QState *sp = P.st + g;
-            const int cS = sp->cS;
-            const int lo = sp->wlo, hi = sp->whi;
-            uint16_t *slot = P.pool + sp->s_off;
-            int i_begin = h ? carry_m[u] : 0;
-            int nh = h ? carry_nh[u] : 0;
-            int m = i_begin;  // first entry >= jhi (half 0: split point)
-            for (int base = i_begin & ~7; base < cS; base += 1024) {
-                uint4 v[4];
-#pragma unroll
-                for (int x = 0; x < 4; x++) {
-                    const int i0 = base + x * 256 + lane * 8;
-                    v[x] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
-                }
-                __syncwarp();
-                bool past = false;
-#pragma unroll
-                for (int x = 0; x < 4; x++) {
-                    const int i0 = base + x * 256 + lane * 8;
-                    const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[x]);
-                    unsigned keepm = 0, inm = 0;
-#pragma unroll
-                    for (int y = 0; y < 8; y++) {
-                        const int i = i0 + y;
-                        const uint32_t j = e8[y];
-                        if (i >= i_begin && i < cS && j >= jlo && j < jhi) {
-                            inm |= 1u << y;
-                            const int pk = (int)prow[j - jlo];
-                            if (pk >= lo && pk < hi) keepm |= 1u << y;
-                        }
-                    }
-                    const int kc = __popc(keepm);
-                    const int inc = warp_incl_scan(kc, lane);
-                    const int tot = __shfl_sync(FULL, inc, 31);
-                    int o = nh + inc - kc;
-#pragma unroll
-                    for (int y = 0; y < 8; y++)
-                        if ((keepm >> y) & 1u) slot[o++] = e8[y];
-                    nh += tot;
-                    m += __reduce_add_sync(FULL, __popc(inm));
-                    // half 0 stops at the first entry of the second half
-                    bool beyond = false;
-#pragma unroll
-                    for (int y = 0; y < 8; y++)
-                        beyond |= (i0 + y < cS && e8[y] >= jhi);
-                    past = __any_sync(FULL, beyond) || past;
-                }
-                __syncwarp();
-                if (past) break;
+            for (int k = 0; k < 4; k++) {
+                const int i0 = base + k * 256 + lane * 8;
+                v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
             }
-            if (h == 0) {
-                carry_m[u] = m;
-                carry_nh[u] = nh;
-                continue;
+            uint32_t keep4 = 0;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int i0 = base + k * 256 + lane * 8;
+                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
+                uint16_t pk[8];
+#pragma unroll
+                for (int x = 0; x < 8; x++) pk[x] = (i0 + x < cS) ? __ldg(prow + e8[x]) : (uint16_t)0xffff;
+#pragma unroll
+                for (int x = 0; x < 8; x++)
+                    if (i0 + x < cS && (int)pk[x] >= lo && (int)pk[x] < hi) keep4 |= 1u << (8 * k + x);
             }
-            // both halves done: update the query (lane 0)
-            if (lane == 0) {
-                sp->tests += cS;
-                sp->exact += 1;
-                const int rings = sp->rings + 1;
-                sp->rings = rings;
-                int status = ST_DONE;  // nh == 0: search.py:136-137 rollback
-                if (nh > 0) {
-                    sp->cS = nh;
-                    int uu[BULK_U];
-                    int nu = 0;
-                    const int nu0 = sp->nu, km = sp->ukeep;
-                    for (int q2 = 0; q2 < nu0; q2++)
-                        if ((km >> q2) & 1) uu[nu++] = sp->u[q2];
-                    bool pin = false;
-                    for (int q2 = 0; q2 < nu; q2++) pin |= uu[q2] == P.prev[g];
-                    sp->p_in = pin;
-                    if (nh >= P.L && rings < P.max_rings && nh - nu > 0) {
-                        int upos[BULK_U];
-                        for (int q2 = 0; q2 < nu; q2++) upos[q2] = lower_bound_u16(slot, nh, (uint32_t)uu[q2]);
-                        Pcg64 rng;
-                        rng.sh = sp->sh;
-                        rng.sl = sp->sl;
-                        rng.ih = sp->ih;
-                        rng.il = sp->il;
-                        rng.has = sp->rng_has;
-                        rng.buf = sp->rng_buf;
-                        const int kk = (int)pcg_integers(rng, (uint64_t)(nh - nu));
-                        const int pos = avail_pos(kk, upos, nu);
-                        if (nu >= BULK_U) {
-                            status = ST_HEAVY;
-                            P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
-                        } else {
-                            const int an = (int)slot[pos];
-                            sp->anchor = an;
-                            uu[nu++] = an;
-                            sp->sh = rng.sh;
-                            sp->sl = rng.sl;
-                            sp->rng_has = rng.has;
-                            sp->rng_buf = rng.buf;
-                            status = ST_ACTIVE;
-                            P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
-                        }
-                    }
-                    for (int q2 = 0; q2 < nu; q2++) sp->u[q2] = uu[q2];
-                    sp->nu = nu;
-                }
-                sp->status = status;
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if (base + k * 256 >= cS) break;
+                const unsigned keepm = (keep4 >> (8 * k)) & 0xffu;
+                const int kc = __popc(keepm);
+                const int inc = warp_incl_scan(kc, lane);
+                const int tot = __shfl_sync(FULL, inc, 31);
+                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
+                int o = nh + inc - kc;
+#pragma unroll
+                for (int x = 0; x < 8; x++)
+                    if ((keepm >> x) & 1u) slot[o++] = e8[x];
+                nh += tot;
             }
             __syncwarp();
         }
-        (void)a;
-        __syncthreads();  // slot k % 3 is free again
-        if (threadIdx.x == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(k + 3);
+        if (lane == 0) {
+            sp->fres = nh;
+            sp->status = ST_FILTERED;
         }
     }
 }

@@ -189,7 +189,7 @@ struct riann_ctx {
     bool bulk_disabled = false;
     // bulk-path frame buffers
     DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_grouped,
-        b_scan_tmp, overflow2, b_item_counts, b_item_starts, b_items;
+        b_scan_tmp, overflow2;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -290,9 +290,6 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     RET(c->b_counters.ensure(64));
     RET(c->b_counts.ensure((size_t)(n + 1) * 4));
     RET(c->b_starts.ensure((size_t)(n + 1) * 4));
-    RET(c->b_item_counts.ensure((size_t)(n + 1) * 4));
-    RET(c->b_item_starts.ensure((size_t)(n + 1) * 4));
-    RET(c->b_items.ensure((size_t)(QN + n + 1) * 16));
     size_t scan_bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, c->b_counts.as<int32_t>(), c->b_starts.as<int32_t>(),
                                      (int)(n + 1), c->stream));
@@ -336,9 +333,6 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.starts = c->b_starts.as<int32_t>();
     B.grouped = c->b_grouped.as<int32_t>();
     B.item_next = ctr + 3;
-    B.item_counts = c->b_item_counts.as<int32_t>();
-    B.item_starts = c->b_item_starts.as<int32_t>();
-    B.items = c->b_items.as<int4>();
     B.out_idx = Pq.out_idx;
     B.out_dist = Pq.out_dist;
     B.stats = Pq.stats;
@@ -381,42 +375,26 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cudaEventRecord(c->ev_heavy, c->stream2));
     B.heavy = c->b_heavy2.as<int32_t>();
     B.n_heavy = ctr + 6;
-    // ring phases: window/draw pass (warp per query) -> counting sort by
-    // anchor -> filter pass in anchor order; a last window pass applies the
-    // final intersection
-    auto wk = rb::bulk_window_kernel<D>;
-    int win_bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&win_bps, wk, 256, 0));
-    const unsigned win_grid = (unsigned)(c->sms * std::max(win_bps, 1));
-    auto rk = rb::bulk_ring_kernel;
+    // ring phases
+    auto rk = rb::bulk_ring_kernel<D>;
     int ring_bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ring_bps, rk, 256, 0));
     const unsigned ring_grid = (unsigned)(c->sms * std::max(ring_bps, 1));
     const unsigned small_grid = (unsigned)c->sms * 4;
     const int phases = Pq.max_rings - 1;
-    // lists: P0 wrote its queries (first anchor drawn) to active[0]
-    int cur = 0;  // list holding the queries to process next
-    for (int ph = 0; ph <= phases; ph++) {
-        const int nxt = cur ^ 1;
-        const bool last = ph == phases;
-        if (ph >= 16 && !last) {  // long ring caps: stop once no query is left
+    for (int ph = 0; ph < phases; ph++) {
+        const int in = ph & 1, out = in ^ 1;
+        B.active_in = c->b_active[in].as<int32_t>();
+        B.n_active_in = ctr + in;
+        B.active_out = c->b_active[out].as<int32_t>();
+        B.n_active_out = ctr + out;
+        if (ph >= 15) {  // long ring caps: stop once no query is left
             int32_t h = 0;
-            CK(cudaMemcpyAsync(&h, ctr + cur, 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(&h, ctr + in, 4, cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
             if (h == 0) break;
         }
-        B.active_in = c->b_active[cur].as<int32_t>();
-        B.n_active_in = ctr + cur;
-        B.active_out = c->b_active[nxt].as<int32_t>();
-        B.n_active_out = ctr + nxt;
-        CK(cudaMemsetAsync(ctr + nxt, 0, 4, c->stream));
-        wk<<<win_grid, 256, 0, c->stream>>>(B, last ? 1 : 0);
-        CK(cudaGetLastError());
-        c->launches += 1;
-        if (last) break;
-        // filter the queries that drew an anchor (list nxt), grouped by anchor
-        B.active_in = c->b_active[nxt].as<int32_t>();
-        B.n_active_in = ctr + nxt;
+        CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
         CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
@@ -428,7 +406,6 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         rk<<<ring_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
         c->launches += 3;
-        cur = nxt;
     }
     // final scan of the light queries (PCA-basis screening)
     {
@@ -824,8 +801,7 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->b_heavy2, &c->overflow2,
-                      &c->b_item_counts, &c->b_item_starts, &c->b_items, &c->pca_T, &c->refs_pca16, &c->e16p,
+                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
                       &c->units_pca, &c->e16max, &c->snap_idx, &c->snap_units, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,

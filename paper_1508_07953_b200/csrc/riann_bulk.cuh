@@ -29,7 +29,7 @@ constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 constexpr int PH_WARPS = 16;     // warps per ring-phase CTA
 constexpr int PH_CHUNK = 64;     // queries per ring-phase work item
 
-enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2, ST_FILTERED = 3 };
+enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
 
 struct __align__(16) QState {
     double d_prev;
@@ -38,8 +38,7 @@ struct __align__(16) QState {
     int32_t cS, first, rings, status;
     int32_t anchor, nu, rng_has, p_in;
     uint32_t rng_buf;
-    int32_t tests, exact, wlo;  // [wlo, whi): the current anchor's window
-    int32_t whi, ukeep, fres, pad1;  // ukeep: used anchors in the ring (mask); fres: |S n ring|
+    int32_t tests, exact, pad;
     int32_t u[BULK_U];
 };
 
@@ -79,9 +78,6 @@ struct BulkParams {
     int32_t *starts;         // exclusive scan of counts
     int32_t *grouped;        // active queries grouped by anchor
     int32_t *item_next;      // work-item counter
-    int32_t *item_counts;    // per anchor row: ceil(count / PH_CHUNK)
-    int32_t *item_starts;    // exclusive scan of item_counts (n + 1)
-    int4 *items;             // (anchor, first grouped entry, count, 0)
     int32_t *out_idx;
     double *out_dist;
     unsigned long long *stats;
@@ -410,132 +406,43 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigne
 }
 
 // ---------------------------------------------------------------------------
-// Ring phase, part 1 ("window"): warp per query of the previous phase's list.
-// Applies the previous intersection (search.py:134-138: rings += 1, rollback
-// on empty, S = S'), tests the loop condition (search.py:121), draws the next
-// anchor (search.py:122-130, numpy RNG) and computes its exact distance
-// (numpy order) and window [wlo, whi) on the anchor's sorted row.  Queries
-// that continue go to active_out.  apply_only: the ring cap is reached.
+// Ring phase: one warp per (query, anchor), queries taken in anchor order so
+// the ~200 anchor rank rows in flight at any time stay resident in L2 (a row
+// is read from HBM about once per phase); membership tests are 8-deep
+// independent lookups pos[a][j] per lane.
 template <int D>
-__global__ void __launch_bounds__(256) bulk_window_kernel(BulkParams P, int apply_only)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t n = P.n;
-    const int m = *P.n_active_in;
-    for (int64_t i = gwarp; i < m; i += nwarps) {
-        const int64_t g = P.active_in[i];
-        QState *sp = P.st + g;
-        int go = 1, a = 0;
-        if (lane == 0) {
-            a = sp->anchor;
-            if (sp->status == ST_FILTERED) {
-                const int cS = sp->cS, nh = sp->fres;
-                sp->tests += cS;
-                sp->exact += 1;
-                const int rings = sp->rings + 1;
-                sp->rings = rings;
-                go = 0;
-                int status = ST_DONE;  // nh == 0: rollback, keep S
-                if (nh > 0) {
-                    sp->cS = nh;
-                    const uint16_t *slot = P.pool + sp->s_off;
-                    int uu[BULK_U];
-                    int nu = 0;
-                    const int nu0 = sp->nu, km = sp->ukeep;
-                    for (int q2 = 0; q2 < nu0; q2++)
-                        if ((km >> q2) & 1) uu[nu++] = sp->u[q2];
-                    bool pin = false;
-                    for (int q2 = 0; q2 < nu; q2++) pin |= uu[q2] == P.prev[g];
-                    sp->p_in = pin;
-                    if (!apply_only && nh >= P.L && rings < P.max_rings && nh - nu > 0) {
-                        int upos[BULK_U];
-                        for (int q2 = 0; q2 < nu; q2++) upos[q2] = lower_bound_u16(slot, nh, (uint32_t)uu[q2]);
-                        Pcg64 rng;
-                        rng.sh = sp->sh;
-                        rng.sl = sp->sl;
-                        rng.ih = sp->ih;
-                        rng.il = sp->il;
-                        rng.has = sp->rng_has;
-                        rng.buf = sp->rng_buf;
-                        const int kk = (int)pcg_integers(rng, (uint64_t)(nh - nu));
-                        const int pos = avail_pos(kk, upos, nu);
-                        if (nu >= BULK_U) {
-                            status = ST_HEAVY;
-                            P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
-                        } else {
-                            a = (int)slot[pos];
-                            sp->anchor = a;
-                            uu[nu++] = a;
-                            sp->sh = rng.sh;
-                            sp->sl = rng.sl;
-                            sp->rng_has = rng.has;
-                            sp->rng_buf = rng.buf;
-                            status = ST_ACTIVE;
-                            go = 1;
-                        }
-                    }
-                    for (int q2 = 0; q2 < nu; q2++) sp->u[q2] = uu[q2];
-                    sp->nu = nu;
-                }
-                sp->status = status;
-            }
-        }
-        go = __shfl_sync(FULL, go, 0);
-        if (!go) continue;
-        a = __shfl_sync(FULL, a, 0);
-        const float *q = P.units + g * D;
-        const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
-        int64_t lo, hi;
-        window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
-                      __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
-        const int nu = sp->nu;
-        int keep = 0;
-        if (lane < nu) {
-            const int pk = __ldg(P.pos + (int64_t)a * n + sp->u[lane]);
-            keep = pk >= lo && pk < hi;
-        }
-        const unsigned km = __ballot_sync(FULL, keep);
-        if (lane == 0) {
-            sp->wlo = (int32_t)lo;
-            sp->whi = (int32_t)hi;
-            sp->ukeep = (int32_t)km;
-            P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Ring phase, part 2 ("filter"): one warp per query, queries in anchor order
-// with dynamic chunked scheduling so the ~200 anchor rank rows in flight stay
-// L2-resident.  S' = S n ring (search.py:134): lo <= pos[a][j] < hi for every
-// candidate, 8-deep independent lookups per lane, in-place order-preserving
-// compaction.  The result is applied by the next window pass.
-__global__ void __launch_bounds__(256) bulk_ring_kernel(BulkParams P)
+__global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
 {
     const int lane = threadIdx.x & 31;
     const int64_t n = P.n;
     const int m = *P.n_active_in;
-    constexpr int GRAB = 4;
-    int ibase = 0, icnt = 0;
+    // CTA rounds over consecutive (anchor-ordered) entries: one global atomic
+    // per round, one entry per warp.  The entries in flight GPU-wide -- and so
+    // the anchor rank rows that must stay L2-resident -- are one per resident
+    // warp, and queries sharing an anchor run on the same SM (L1 reuse).
+    __shared__ int s_base;
+    const int wpb = blockDim.x >> 5;
     for (;;) {
-        if (icnt == 0) {
-            int b = 0;
-            if (lane == 0) b = atomicAdd(P.item_next, GRAB);
-            ibase = __shfl_sync(FULL, b, 0);
-            icnt = GRAB;
-        }
-        const int i = ibase + (GRAB - icnt);
-        icnt--;
-        if (i >= m) break;
+        __syncthreads();
+        if (threadIdx.x == 0) s_base = atomicAdd(P.item_next, wpb);
+        __syncthreads();
+        const int i = s_base + (int)(threadIdx.x >> 5);
+        if (s_base >= m) break;
+        if (i >= m) continue;
         const int64_t g = P.grouped[i];
         QState *sp = P.st + g;
         const int a = sp->anchor;
         const int cS = sp->cS;
-        const int lo = sp->wlo, hi = sp->whi;
         uint16_t *slot = P.pool + sp->s_off;
+        const float *q = P.units + g * D;
+        // search.py:131-133: exact d_a (numpy order), window on row a
+        const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
+        int64_t lo, hi;
+        window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
+                      __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
         const uint16_t *prow = P.pos + (int64_t)a * n;
+        // search.py:134: S' = S n ring, order kept, filtered in place; per block of
+        // 1024 entries all list loads, then all rank lookups, are issued together
         int nh = 0;
         for (int base = 0; base < cS; base += 1024) {
             uint4 v[4];
@@ -544,7 +451,7 @@ __global__ void __launch_bounds__(256) bulk_ring_kernel(BulkParams P)
                 const int i0 = base + k * 256 + lane * 8;
                 v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
             }
-            uint32_t keep4 = 0;
+            uint32_t keep4 = 0;  // 8 bits per k
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const int i0 = base + k * 256 + lane * 8;
@@ -554,7 +461,7 @@ __global__ void __launch_bounds__(256) bulk_ring_kernel(BulkParams P)
                 for (int x = 0; x < 8; x++) pk[x] = (i0 + x < cS) ? __ldg(prow + e8[x]) : (uint16_t)0xffff;
 #pragma unroll
                 for (int x = 0; x < 8; x++)
-                    if (i0 + x < cS && (int)pk[x] >= lo && (int)pk[x] < hi) keep4 |= 1u << (8 * k + x);
+                    if (i0 + x < cS && pk[x] >= lo && pk[x] < hi) keep4 |= 1u << (8 * k + x);
             }
             __syncwarp();
 #pragma unroll
@@ -574,9 +481,57 @@ __global__ void __launch_bounds__(256) bulk_ring_kernel(BulkParams P)
             __syncwarp();
         }
         if (lane == 0) {
-            sp->fres = nh;
-            sp->status = ST_FILTERED;
+            sp->tests += cS;
+            sp->exact += 1;
+            const int rings = sp->rings + 1;
+            sp->rings = rings;
+            int status = ST_DONE;  // nh == 0: search.py:136-137 rollback
+            if (nh > 0) {
+                sp->cS = nh;
+                int u[BULK_U];
+                int nu = 0;
+                const int nu0 = sp->nu;
+                for (int k = 0; k < nu0; k++) {
+                    const int uk = sp->u[k];
+                    const int pk = __ldg(prow + uk);
+                    if (pk >= lo && pk < hi) u[nu++] = uk;
+                }
+                bool pin = false;
+                for (int k = 0; k < nu; k++) pin |= u[k] == P.prev[g];
+                sp->p_in = pin;
+                if (nh >= P.L && rings < P.max_rings && nh - nu > 0) {
+                    int upos[BULK_U];
+                    for (int k = 0; k < nu; k++) upos[k] = lower_bound_u16(slot, nh, (uint32_t)u[k]);
+                    Pcg64 rng;
+                    rng.sh = sp->sh;
+                    rng.sl = sp->sl;
+                    rng.ih = sp->ih;
+                    rng.il = sp->il;
+                    rng.has = sp->rng_has;
+                    rng.buf = sp->rng_buf;
+                    const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
+                    const int pos = avail_pos(k, upos, nu);
+                    if (nu >= BULK_U) {
+                        status = ST_HEAVY;
+                        P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
+                    } else {
+                        const int an = (int)slot[pos];
+                        sp->anchor = an;
+                        u[nu++] = an;
+                        sp->sh = rng.sh;
+                        sp->sl = rng.sl;
+                        sp->rng_has = rng.has;
+                        sp->rng_buf = rng.buf;
+                        status = ST_ACTIVE;
+                        P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+                    }
+                }
+                for (int k = 0; k < nu; k++) sp->u[k] = u[k];
+                sp->nu = nu;
+            }
+            sp->status = status;
         }
+        __syncwarp();
     }
 }
 

@@ -287,7 +287,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     RET(c->b_heavy.ensure((size_t)QN * 4));
     RET(c->b_heavy2.ensure((size_t)QN * 4));
     RET(c->b_grouped.ensure((size_t)QN * 4));
-    RET(c->b_counters.ensure(64));
+    RET(c->b_counters.ensure(256));
     RET(c->b_counts.ensure((size_t)(n + 1) * 4));
     RET(c->b_starts.ensure((size_t)(n + 1) * 4));
     size_t scan_bytes = 0;
@@ -296,7 +296,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     RET(c->b_scan_tmp.ensure(scan_bytes));
     // [0..1] active counts, [2] P0 heavy, [3] item counter, [4..5] pool top, [6] ring heavy
     int32_t *ctr = c->b_counters.as<int32_t>();
-    CK(cudaMemsetAsync(ctr, 0, 64, c->stream));
+    CK(cudaMemsetAsync(ctr, 0, 256, c->stream));
 
     rb::BulkParams B;
     memset(&B, 0, sizeof B);
@@ -333,6 +333,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.starts = c->b_starts.as<int32_t>();
     B.grouped = c->b_grouped.as<int32_t>();
     B.item_next = ctr + 3;
+    B.seg_next = ctr + 16;
     B.out_idx = Pq.out_idx;
     B.out_dist = Pq.out_dist;
     B.stats = Pq.stats;
@@ -396,6 +397,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         }
         CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
         CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
+        CK(cudaMemsetAsync(ctr + 16, 0, 16 * 4, c->stream));
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());

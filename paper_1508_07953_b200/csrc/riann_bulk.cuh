@@ -78,6 +78,7 @@ struct BulkParams {
     int32_t *starts;         // exclusive scan of counts
     int32_t *grouped;        // active queries grouped by anchor
     int32_t *item_next;      // work-item counter
+    int32_t *seg_next;       // 16 segment counters (ring phase scheduling)
     int32_t *out_idx;
     double *out_dist;
     unsigned long long *stats;
@@ -416,19 +417,30 @@ __global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
     const int lane = threadIdx.x & 31;
     const int64_t n = P.n;
     const int m = *P.n_active_in;
-    // CTA rounds over consecutive (anchor-ordered) entries: one global atomic
-    // per round, one entry per warp.  The entries in flight GPU-wide -- and so
-    // the anchor rank rows that must stay L2-resident -- are one per resident
-    // warp, and queries sharing an anchor run on the same SM (L1 reuse).
-    __shared__ int s_base;
-    const int wpb = blockDim.x >> 5;
+    // One entry per grab keeps the entries in flight GPU-wide -- and so the
+    // anchor rank rows that must stay L2-resident -- at one per resident warp.
+    // The anchor-ordered list is cut into NSEG segments with their own
+    // counters (atomic traffic / NSEG); a warp whose segment is exhausted
+    // steals from the next ones.
+    constexpr int NSEG = 16;
+    const int64_t gw0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int seg = (int)(gw0 % NSEG), tried = 0;
     for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_base = atomicAdd(P.item_next, wpb);
-        __syncthreads();
-        const int i = s_base + (int)(threadIdx.x >> 5);
-        if (s_base >= m) break;
-        if (i >= m) continue;
+        int i = -1;
+        if (lane == 0) {
+            while (tried < NSEG) {
+                const int s0 = (int)((int64_t)m * seg / NSEG), s1 = (int)((int64_t)m * (seg + 1) / NSEG);
+                const int t = s0 + atomicAdd(P.seg_next + seg, 1);
+                if (t < s1) {
+                    i = t;
+                    break;
+                }
+                seg = (seg + 1) % NSEG;
+                tried++;
+            }
+        }
+        i = __shfl_sync(FULL, i, 0);
+        if (i < 0) break;
         const int64_t g = P.grouped[i];
         QState *sp = P.st + g;
         const int a = sp->anchor;

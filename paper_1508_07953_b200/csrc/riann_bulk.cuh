@@ -173,63 +173,6 @@ __device__ __forceinline__ void window_coarse(const float *__restrict__ row, con
     hi = __shfl_sync(FULL, res, 16);
 }
 
-// Same result as window_coarse with two dependent round trips: the whole
-// coarse row (nb <= 1024 entries) is read at once and counted (the rows are
-// sorted, so predicate counts are positions), then both <= COARSE-entry fine
-// segments are read together and counted.
-__device__ __forceinline__ void window_flat(const float *__restrict__ row, const float *__restrict__ cs, int nb,
-                                            int64_t n, double lv, double hv, int lane, int64_t &lo, int64_t &hi)
-{
-    int clt = 0, cle = 0;
-    for (int i0 = 0; i0 < nb; i0 += 1024) {
-        float v[32];
-#pragma unroll
-        for (int x = 0; x < 8; x++) {
-            const int i = i0 + x * 128 + lane * 4;
-            if (i + 3 < nb && ((reinterpret_cast<uintptr_t>(cs) & 15u) == 0)) {
-                const float4 f = __ldg(reinterpret_cast<const float4 *>(cs + i));
-                v[4 * x] = f.x;
-                v[4 * x + 1] = f.y;
-                v[4 * x + 2] = f.z;
-                v[4 * x + 3] = f.w;
-            } else {
-#pragma unroll
-                for (int y = 0; y < 4; y++) v[4 * x + y] = i + y < nb ? __ldg(cs + i + y) : __int_as_float(0x7f800000);
-            }
-        }
-#pragma unroll
-        for (int x = 0; x < 32; x++) {
-            const double dv = (double)v[x];
-            clt += dv < lv ? 1 : 0;
-            cle += dv <= hv ? 1 : 0;
-        }
-    }
-    clt = __reduce_add_sync(FULL, clt);
-    cle = __reduce_add_sync(FULL, cle);
-    const int64_t a0 = clt > 0 ? (int64_t)(clt - 1) * COARSE + 1 : 0;
-    const int64_t a1 = (clt < nb) ? (int64_t)clt * COARSE : n;
-    const int64_t b0 = cle > 0 ? (int64_t)(cle - 1) * COARSE + 1 : 0;
-    const int64_t b1 = (cle < nb) ? (int64_t)cle * COARSE : n;
-    // each fine segment has < COARSE (64) entries: two per lane
-    float fa[2], fb[2];
-#pragma unroll
-    for (int x = 0; x < 2; x++) {
-        const int64_t ka = a0 + x * 32 + lane, kb = b0 + x * 32 + lane;
-        fa[x] = ka < a1 ? __ldg(row + ka) : __int_as_float(0x7f800000);
-        fb[x] = kb < b1 ? __ldg(row + kb) : __int_as_float(0x7f800000);
-    }
-    int ca = 0, cb = 0;
-#pragma unroll
-    for (int x = 0; x < 2; x++) {
-        ca += (double)fa[x] < lv ? 1 : 0;
-        cb += (double)fb[x] <= hv ? 1 : 0;
-    }
-    for (int64_t k = a0 + 64 + lane; k < a1; k += 32) ca += (double)__ldg(row + k) < lv ? 1 : 0;
-    for (int64_t k = b0 + 64 + lane; k < b1; k += 32) cb += (double)__ldg(row + k) <= hv ? 1 : 0;
-    lo = a0 + __reduce_add_sync(FULL, ca);
-    hi = b0 + __reduce_add_sync(FULL, cb);
-}
-
 // k-th (0-based) element of ascending list S minus the used anchors u[0..nu)
 // (search.py:122, 129).  upos: positions of the used anchors in S.
 __device__ __forceinline__ int avail_pos(int k, const int *upos, int nu)
@@ -504,30 +447,21 @@ __global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
         const int cS = sp->cS;
         uint16_t *slot = P.pool + sp->s_off;
         const float *q = P.units + g * D;
-        // the first block of the candidate list does not depend on the window:
-        // its loads are issued before the distance / window round trips
-        uint4 v[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int i0 = k * 256 + lane * 8;
-            v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
-        }
         // search.py:131-133: exact d_a (numpy order), window on row a
         const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
         int64_t lo, hi;
-        window_flat(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
-                    __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
+        window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
+                      __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
         const uint16_t *prow = P.pos + (int64_t)a * n;
         // search.py:134: S' = S n ring, order kept, filtered in place; per block of
         // 1024 entries all list loads, then all rank lookups, are issued together
         int nh = 0;
         for (int base = 0; base < cS; base += 1024) {
-            if (base > 0) {
+            uint4 v[4];
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const int i0 = base + k * 256 + lane * 8;
-                    v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
-                }
+            for (int k = 0; k < 4; k++) {
+                const int i0 = base + k * 256 + lane * 8;
+                v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
             }
             uint32_t keep4 = 0;  // 8 bits per k
 #pragma unroll

@@ -641,8 +641,17 @@ int launch_units(riann_ctx *c, const float *frame, int H, int W, int C, float *u
     U.tc = tc;
     if (U.Q <= 0) return 0;
     unsigned blocks = (unsigned)((U.Q + 127) / 128);
-    if (c->pw == 8 && c->ph == 8) rb::units_kernel<8, 8><<<blocks, 128, 0, c->stream>>>(U);
-    else rb::units_kernel<0, 0><<<blocks, 128, 0, c->stream>>>(U);
+    if (c->pw == 8 && c->ph == 8 && c->dim == 64) {
+        const unsigned b = (unsigned)std::min<int64_t>((U.Q + 31) / 32, (int64_t)c->sms * 16);
+        rb::units_warp_kernel<64><<<b, 256, 0, c->stream>>>(U);
+    } else if (c->pw == 8 && c->ph == 8 && c->dim == 192) {
+        const unsigned b = (unsigned)std::min<int64_t>((U.Q + 15) / 16, (int64_t)c->sms * 16);
+        rb::units_warp_kernel<192><<<b, 256, 0, c->stream>>>(U);
+    } else if (c->pw == 8 && c->ph == 8) {
+        rb::units_kernel<8, 8><<<blocks, 128, 0, c->stream>>>(U);
+    } else {
+        rb::units_kernel<0, 0><<<blocks, 128, 0, c->stream>>>(U);
+    }
     CK(cudaGetLastError());
     return 0;
 }

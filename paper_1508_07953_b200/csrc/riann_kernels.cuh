@@ -75,6 +75,64 @@ __global__ void __launch_bounds__(128) units_kernel(UnitsParams P)
     }
 }
 
+// K1, warp-cooperative form for 8x8 patches with D = 64 * C in {64, 192}:
+// lane (h, dx) of a Lay<D>::G-lane group owns numpy's pairwise accumulator dx
+// of half h, so the squared norm and the temporal-change distance come out of
+// the same xor tree as exact_dist; unit rows are written by the group with
+// 32-byte runs per step.  One group per grid position.
+template <int D>
+__global__ void __launch_bounds__(256) units_warp_kernel(UnitsParams P)
+{
+    constexpr int G = Lay<D>::G, PER = Lay<D>::PER, NG = WARP / G;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const int64_t grp_global = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NG + lane / G;
+    const int64_t ngroups = (((int64_t)gridDim.x * blockDim.x) >> 5) * NG;
+    const int base = Lay<D>::base(gl);
+    for (int64_t g0 = grp_global - lane / G; g0 < P.Q; g0 += ngroups) {
+        const int64_t g = g0 + lane / G;
+        const bool valid = g < P.Q;
+        const int64_t gg = valid ? g : 0;
+        const int x = (int)(gg % P.gw), y = (int)(gg / P.gw);
+        float v[PER];
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+            const int e = base + 8 * i;
+            const int c = e >> 6, dy = (e >> 3) & 7, dx = e & 7;
+            v[i] = __ldg(P.frame + ((int64_t)(y + dy) * P.W + (x + dx)) * P.C + c);
+        }
+        double acc = __dmul_rn((double)v[0], (double)v[0]);
+#pragma unroll
+        for (int i = 1; i < PER; i++) acc = __dadd_rn(acc, __dmul_rn((double)v[i], (double)v[i]));
+        acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
+        acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
+        acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
+        if (G == 16) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 8));
+        const double nr = __dsqrt_rn(acc);
+        const bool ok = nr >= 1e-12;
+        float u[PER];
+#pragma unroll
+        for (int i = 0; i < PER; i++) u[i] = ok ? __double2float_rn(__ddiv_rn((double)v[i], nr)) : 0.0f;
+        if (valid) {
+            float *ur = P.unit + g * D + base;
+#pragma unroll
+            for (int i = 0; i < PER; i++) ur[8 * i] = u[i];
+            if (P.norms && gl == 0) P.norms[g] = ok ? nr : 0.0;
+        }
+        if (P.tc) {
+            const float *pr = P.prev_unit + gg * D + base;
+            double t = sqdiff(u[0], __ldg(pr));
+#pragma unroll
+            for (int i = 1; i < PER; i++) t = __dadd_rn(t, sqdiff(u[i], __ldg(pr + 8 * i)));
+            t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 1));
+            t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 2));
+            t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 4));
+            if (G == 16) t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 8));
+            if (valid && gl == 0) P.tc[g] = __dsqrt_rn(t);
+        }
+    }
+}
+
 // normalize_rows on explicit rows (patches.py:100-115); T = float or double
 // input (the reference converts any input to float64 first).
 template <class T>

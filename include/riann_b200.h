@@ -74,9 +74,10 @@ void *riann_ctx_stream(riann_ctx *ctx);
 int riann_sync(riann_ctx *ctx);
 /* device bytes currently held by the context */
 uint64_t riann_ctx_device_bytes(riann_ctx *ctx);
-/* Frame-path selection: 0 = auto (anchor-grouped phases when n <= 65,536 and
- * dim is 64 or 192, per-query kernel otherwise), 1 = per-query kernel only.
- * Both produce identical results; the switch exists for testing. */
+/* Path selection mask: 0 = auto (anchor-grouped frame phases when n <= 65,536
+ * and dim is 64 or 192; tensor-core exact comparator for dim 64 / 192);
+ * bit 1 = per-query frame kernel only; bit 2 = SIMT exact comparator.
+ * All paths produce identical results; the switch exists for testing. */
 int riann_ctx_set_path(riann_ctx *ctx, int path);
 
 /* ---- model (model.py:56-83 ReferenceModel) ----------------------------- */
@@ -163,8 +164,18 @@ int riann_query_batch(riann_ctx *ctx, const float *queries, const int32_t *prev,
                       int64_t *scanned_len);
 
 /* ---- exact comparator (evaluation.py:24-50) ----------------------------- */
+/* Exact nearest reference per query: index of the first minimum of the
+ * float64 distances (numpy argmin), bit-identical to exact_nn.  For dim 64
+ * and 192 the distances are screened on the tensor cores (tcgen05 bf16x3
+ * split GEMM with rigorous bounds) and the survivors re-evaluated in float64;
+ * riann_ctx_set_path bit 2 selects the SIMT full scan instead. */
 int riann_exact_nn_batch(riann_ctx *ctx, const float *queries, int64_t m,
                          int32_t *out_idx, double *out_dist);
+/* Same on device buffers, asynchronous on the context stream.  stats (may be
+ * NULL; synchronises): [0] float64 re-checks, [1] queries that took the full
+ * exact scan (screen list overflow). */
+int riann_exact_nn_device(riann_ctx *ctx, const float *queries, int64_t m,
+                          int32_t *out_idx, double *out_dist, uint64_t *stats);
 int riann_exact_field(riann_ctx *ctx, const float *frame, int H, int W, int C,
                       int32_t *out_idx, double *out_dist);
 

@@ -71,6 +71,7 @@ SIGNATURES = {
     "riann_ring_candidates": (i32, [P, i64, dbl, dbl, C.POINTER(i64), C.POINTER(i64), P]),
     "riann_query_batch": (i32, [P, P, P, P, P, i64, i32, dbl, i32, P, P, P, P, P, P, P, P]),
     "riann_exact_nn_batch": (i32, [P, P, i64, P, P]),
+    "riann_exact_nn_device": (i32, [P, P, i64, P, P, P]),
     "riann_exact_field": (i32, [P, P, i32, i32, i32, P, P]),
     "riann_init_field": (i32, [i32, i32, i64, P, i32, P]),
     "riann_pairwise_sum": (dbl, [P, i64]),
@@ -208,8 +209,10 @@ def context(device: int | None = None) -> Context:
 
 
 def set_frame_path(path: int, device: int | None = None) -> None:
-    """0 = auto (anchor-grouped phases where supported), 1 = per-query kernel
-    only.  Results are identical; this exists for testing and measurement."""
+    """Path mask: 0 = auto (anchor-grouped frame phases, tensor-core exact
+    comparator where supported); 1 = per-query frame kernel only; 2 = SIMT
+    exact comparator.  Results are identical; this exists for testing and
+    measurement."""
     ctx = context(device)
     with ctx.lock:
         check(lib().riann_ctx_set_path(ctx.h, int(path)))

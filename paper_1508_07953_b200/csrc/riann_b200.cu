@@ -23,6 +23,7 @@
 
 #include "riann_b200.h"
 #include "riann_bulk.cuh"
+#include "riann_exact_tc.cuh"
 
 namespace {
 
@@ -187,6 +188,10 @@ struct riann_ctx {
     cublasHandle_t cublas = nullptr;
     int ncoarse = 0;
     bool bulk_disabled = false;
+    // K4 tensor-core comparator: split reference operand, norms, per-call scratch
+    bool exact_simt = false, x_ready = false;
+    DevBuf x_B, x_nr, x_center, x_A, x_nq, x_cand, x_lb, x_ncand, x_ub, x_fb, x_q, x_idx, x_dist;
+    uint64_t x_checked = 0, x_fallback = 0;
     // bulk-path frame buffers
     DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_grouped,
         b_scan_tmp, overflow2;
@@ -232,7 +237,8 @@ struct riann_ctx {
         uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + pos.cap + coarse.cap + b_state.cap + pca_T.cap +
                      refs_pca16.cap + e16p.cap + units_pca.cap +
                      b_pool.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
-                     fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap;
+                     fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap + x_B.cap + x_A.cap +
+                     x_cand.cap + x_lb.cap;
         return b;
     }
 };
@@ -818,7 +824,9 @@ int riann_ctx_destroy(riann_ctx *c)
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
                       &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,
                       &c->tree.leaf_start, &c->tree.leaf_len, &c->tree.leaf_node, &c->tree.level_off,
-                      &c->tree.inner, &c->tree.left, &c->tree.right, &c->tree.node_val};
+                      &c->tree.inner, &c->tree.left, &c->tree.right, &c->tree.node_val, &c->x_B, &c->x_nr, &c->x_center,
+                      &c->x_A, &c->x_nq, &c->x_cand, &c->x_lb, &c->x_ncand, &c->x_ub, &c->x_fb, &c->x_q,
+                      &c->x_idx, &c->x_dist};
     for (DevBuf *b : bufs) b->release();
     for (auto &a : c->ev_pending)
         for (auto e : a) cudaEventDestroy(e);
@@ -848,8 +856,10 @@ uint64_t riann_ctx_device_bytes(riann_ctx *c) { return c ? c->bytes() : 0; }
 int riann_ctx_set_path(riann_ctx *c, int path)
 {
     if (!c) return fail(RIANN_E_STATE, "null context");
-    if (path < 0 || path > 1) return fail(RIANN_E_VALUE, "path must be 0 (auto) or 1 (per-query kernel)");
-    c->bulk_disabled = path == 1;
+    if (path < 0 || path > 3)
+        return fail(RIANN_E_VALUE, "path must be a mask of 1 (per-query frame kernel) and 2 (SIMT exact comparator)");
+    c->bulk_disabled = (path & 1) != 0;
+    c->exact_simt = (path & 2) != 0;
     return 0;
 }
 
@@ -871,6 +881,7 @@ int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, in
     c->pos.release();
     c->coarse.release();
     c->tables = false;
+    c->x_ready = false;
     RET(c->refs.ensure((size_t)n * dim * 4));
     CK(cudaMemcpyAsync(c->refs.p, refs, (size_t)n * dim * 4, cudaMemcpyHostToDevice, c->stream));
     RET(c->refs16.ensure((size_t)n * dim * 2));
@@ -1501,26 +1512,170 @@ int riann_query_batch(riann_ctx *c, const float *queries, const int32_t *prev, c
     return 0;
 }
 
+}  // extern "C"
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D bf16 operand (rows, kcols), K-major, 64 x 128 boxes with the 128-byte swizzle
+int encode_operand(CUtensorMap *map, const void *base, int64_t rows, int kcols)
+{
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) return fail(RIANN_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)p;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)kcols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kcols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)rb::tc::BK, (cuuint32_t)rb::tc::BM};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(RIANN_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return 0;
+}
+
+// |d2_est - d2| <= E * (||q||^2 + ||r||^2) for the 3-term bf16 split with K = 3D:
+//   split residual   <= 3.1 * 2^-16 * ||q|| ||r||
+//   fp32 accumulation <= 2K * 2^-23 * 1.02 ||q|| ||r||  (4x the round-to-nearest gamma_K, for truncating adders)
+//   norms + d2 arithmetic in float <= 8 * 2^-24 * (||q||^2 + ||r||^2)
+//   centring rounding (|fl(x-c) - (x-c)| <= 2^-24 |fl(x-c)|) <= 5 * 2^-24 * (||q||^2 + ||r||^2)
+// with q, r the centred rows, and 2 ||q|| ||r|| <= ||q||^2 + ||r||^2.  Rounded up generously.
+float exact_eps(int K) { return (float)(4.0 * std::ldexp(1.0, -16) + 2.1 * K * std::ldexp(1.0, -23) + std::ldexp(1.0, -19)); }
+
+// fallback list (m int32) then the counters [fallbacks i32, pad, checked u64], 16-byte aligned
+size_t fb_counters_off(int64_t m) { return ((size_t)m * 4 + 15) & ~(size_t)15; }
+
+bool exact_tc_ok(const riann_ctx *c) { return !c->exact_simt && (c->dim == 64 || c->dim == 192); }
+
+template <int D>
+int exact_tc_run(riann_ctx *c, const float *dq, int64_t m, int32_t *didx, double *ddist)
+{
+    namespace T = rb::tc;
+    constexpr int K = 3 * D;
+    const int64_t n = c->n;
+    const unsigned eblocks = (unsigned)c->sms * 8;
+    if (!c->x_ready) {
+        RET(c->x_B.ensure((size_t)n * K * 2));
+        RET(c->x_nr.ensure((size_t)n * 4));
+        RET(c->x_center.ensure((size_t)D * 12));
+        double *cacc = reinterpret_cast<double *>(c->x_center.as<char>() + (size_t)D * 4);
+        CK(cudaMemsetAsync(cacc, 0, (size_t)D * 8, c->stream));
+        T::center_sum_kernel<<<(unsigned)((n + 1023) / 1024), D, 0, c->stream>>>(c->refs.as<float>(), n, D, cacc);
+        T::center_fin_kernel<<<1, D, 0, c->stream>>>(cacc, n, D, c->x_center.as<float>());
+        T::split_kernel<<<eblocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->x_center.as<float>(), n, D, 0,
+                                                        c->x_B.as<__nv_bfloat16>());
+        T::norm2_kernel<<<eblocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->x_center.as<float>(), n, D,
+                                                        c->x_nr.as<float>());
+        CK(cudaGetLastError());
+        c->x_ready = true;
+    }
+    RET(c->x_A.ensure((size_t)m * K * 2));
+    RET(c->x_nq.ensure((size_t)m * 4));
+    RET(c->x_cand.ensure((size_t)m * T::NCAND * 4));
+    RET(c->x_lb.ensure((size_t)m * T::NCAND * 4));
+    RET(c->x_ncand.ensure((size_t)m * 4));
+    RET(c->x_ub.ensure((size_t)m * 4));
+    RET(c->x_fb.ensure(fb_counters_off(m) + 64));
+    T::split_kernel<<<eblocks, 256, 0, c->stream>>>(dq, c->x_center.as<float>(), m, D, 1, c->x_A.as<__nv_bfloat16>());
+    T::norm2_kernel<<<eblocks, 256, 0, c->stream>>>(dq, c->x_center.as<float>(), m, D, c->x_nq.as<float>());
+    CK(cudaGetLastError());
+    CUtensorMap mapA, mapB;
+    RET(encode_operand(&mapA, c->x_A.p, m, K));
+    RET(encode_operand(&mapB, c->x_B.p, n, K));
+    T::ExactParams P{};
+    P.nq = c->x_nq.as<float>();
+    P.nr = c->x_nr.as<float>();
+    P.m = m;
+    P.n = n;
+    P.kblocks = K / T::BK;
+    P.eps = exact_eps(K);
+    P.cand = c->x_cand.as<int32_t>();
+    P.cand_lb = c->x_lb.as<float>();
+    P.ncand = c->x_ncand.as<int32_t>();
+    P.best_ub = c->x_ub.as<float>();
+    const int smem = T::smem_bytes(P.kblocks);
+    CK(cudaFuncSetAttribute(T::exact_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    T::exact_tc_kernel<<<(unsigned)((m + T::BM - 1) / T::BM), 256, smem, c->stream>>>(mapA, mapB, P);
+    CK(cudaGetLastError());
+    int32_t *nfb = reinterpret_cast<int32_t *>(c->x_fb.as<char>() + fb_counters_off(m));
+    unsigned long long *nchk = reinterpret_cast<unsigned long long *>(c->x_fb.as<char>() + fb_counters_off(m) + 8);
+    CK(cudaMemsetAsync(nfb, 0, 16, c->stream));
+    const unsigned rblocks = (unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)c->sms * 16);
+    T::exact_recheck_kernel<D><<<rblocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, dq, m, P.cand, P.cand_lb,
+                                                               P.ncand, P.best_ub, didx, ddist, c->x_fb.as<int32_t>(),
+                                                               nfb, nchk);
+    T::exact_list_kernel<D><<<(unsigned)c->sms * 8, 256, 0, c->stream>>>(c->refs.as<float>(), n, dq,
+                                                                         c->x_fb.as<int32_t>(), nfb, didx, ddist);
+    CK(cudaGetLastError());
+    c->launches += 5;
+    return 0;
+}
+
+// K4 on device buffers: tensor-core screen + exact re-check, or the SIMT scan
+int exact_run(riann_ctx *c, const float *dq, int64_t m, int32_t *didx, double *ddist)
+{
+    if (exact_tc_ok(c)) {
+        if (c->dim == 64) return exact_tc_run<64>(c, dq, m, didx, ddist);
+        return exact_tc_run<192>(c, dq, m, didx, ddist);
+    }
+    const unsigned blocks = (unsigned)((m + 7) / 8 < (int64_t)c->sms * 8 ? (m + 7) / 8 : (int64_t)c->sms * 8);
+    switch (c->dim) {
+    case 16: rb::exact_nn_kernel<16><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq, m, didx, ddist); break;
+    case 64: rb::exact_nn_kernel<64><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq, m, didx, ddist); break;
+    case 192: rb::exact_nn_kernel<192><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq, m, didx, ddist); break;
+    default: rb::exact_nn_kernel<0><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq, m, didx, ddist); break;
+    }
+    CK(cudaGetLastError());
+    c->launches += 1;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int riann_exact_nn_device(riann_ctx *c, const float *queries, int64_t m, int32_t *out_idx, double *out_dist,
+                          uint64_t *stats)
+{
+    RET(check_model(c, false));
+    if (m < 0) return fail(RIANN_E_VALUE, "negative query count");
+    RET(c->use());
+    if (m > 0) RET(exact_run(c, queries, m, out_idx, out_dist));
+    if (stats) {
+        stats[0] = stats[1] = 0;
+        if (m > 0 && exact_tc_ok(c)) {
+            int32_t h[4];
+            CK(cudaMemcpyAsync(h, c->x_fb.as<char>() + fb_counters_off(m), 16, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            unsigned long long chk;
+            std::memcpy(&chk, h + 2, 8);
+            stats[0] = chk;
+            stats[1] = (uint64_t)h[0];
+        }
+    }
+    return 0;
+}
+
 int riann_exact_nn_batch(riann_ctx *c, const float *queries, int64_t m, int32_t *out_idx, double *out_dist)
 {
     RET(check_model(c, false));
     if (m <= 0) return 0;
     RET(c->use());
-    DevBuf dq, di, dd;
-    RET(dq.ensure((size_t)m * c->dim * 4));
-    RET(di.ensure((size_t)m * 4));
-    RET(dd.ensure((size_t)m * 8));
-    CK(cudaMemcpyAsync(dq.p, queries, (size_t)m * c->dim * 4, cudaMemcpyHostToDevice, c->stream));
-    unsigned blocks = (unsigned)((m + 7) / 8 < (int64_t)c->sms * 8 ? (m + 7) / 8 : (int64_t)c->sms * 8);
-    switch (c->dim) {
-    case 16: rb::exact_nn_kernel<16><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
-    case 64: rb::exact_nn_kernel<64><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
-    case 192: rb::exact_nn_kernel<192><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
-    default: rb::exact_nn_kernel<0><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->n, c->dim, dq.as<float>(), m, di.as<int32_t>(), dd.as<double>()); break;
-    }
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(out_idx, di.p, (size_t)m * 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(out_dist, dd.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    RET(c->x_q.ensure((size_t)m * c->dim * 4));
+    RET(c->x_idx.ensure((size_t)m * 4));
+    RET(c->x_dist.ensure((size_t)m * 8));
+    CK(cudaMemcpyAsync(c->x_q.p, queries, (size_t)m * c->dim * 4, cudaMemcpyHostToDevice, c->stream));
+    RET(exact_run(c, c->x_q.as<float>(), m, c->x_idx.as<int32_t>(), c->x_dist.as<double>()));
+    CK(cudaMemcpyAsync(out_idx, c->x_idx.p, (size_t)m * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(out_dist, c->x_dist.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }

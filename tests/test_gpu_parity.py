@@ -321,3 +321,94 @@ def test_frame_paths_identical(R, oracle_mod, path):
                 prev = idx
     finally:
         N.set_frame_path(0)
+
+
+# ---------------------------------------------------------------------------
+# K4 exact comparator: tensor-core screen (tcgen05) + float64 re-check vs the
+# oracle's exact_nn (evaluation.py:24-33) and vs the SIMT full scan.
+def _exact_both_paths(R, queries, model):
+    from paper_1508_07953_b200 import _native as N
+
+    a = R.exact_nn_batch(queries, model)
+    N.set_frame_path(2)
+    try:
+        b = R.exact_nn_batch(queries, model)
+    finally:
+        N.set_frame_path(0)
+    return a, b
+
+
+def _exact_stats(model, queries):
+    import ctypes
+
+    from paper_1508_07953_b200 import _native as N
+    from paper_1508_07953_b200.evaluation import _upload_refs
+
+    import torch
+
+    q = torch.from_numpy(np.ascontiguousarray(queries, np.float32)).cuda()
+    idx = torch.empty(q.shape[0], dtype=torch.int32, device="cuda")
+    dist = torch.empty(q.shape[0], dtype=torch.float64, device="cuda")
+    st = (ctypes.c_uint64 * 2)()
+    ctx = N.context()
+    with ctx.lock:
+        _upload_refs(ctx, model)
+        torch.cuda.synchronize()
+        N.check(N.lib().riann_exact_nn_device(ctx.h, q.data_ptr(), q.shape[0], idx.data_ptr(), dist.data_ptr(), st))
+        N.check(N.lib().riann_sync(ctx.h))
+    return idx.cpu().numpy(), dist.cpu().numpy(), int(st[0]), int(st[1])
+
+
+@pytest.mark.parametrize("dim,patch,ch", [(64, (8, 8), 1), (192, (8, 8), 3)])
+@pytest.mark.parametrize("n,m", [(1, 5), (7, 130), (1000, 1001), (4096, 3000)])
+def test_exact_tc_vs_oracle(R, oracle_mod, dim, patch, ch, n, m):
+    rng = np.random.default_rng(dim * 7 + n)
+    refs, _ = R.normalize_rows(rng.standard_normal((n, dim)).astype(np.float32))
+    q, _ = R.normalize_rows(rng.standard_normal((m, dim)).astype(np.float32))
+    q[: min(m, n) // 2] = refs[: min(m, n) // 2]           # exact hits (distance 0)
+    model = R.ReferenceModel.from_refs(refs, patch, channels=ch)
+    want_i, want_d = oracle_mod.exact_nn_batch(refs, q)
+    (ai, ad), (bi, bd) = _exact_both_paths(R, q, model)
+    assert np.array_equal(ai, want_i) and np.array_equal(_bits(ad), _bits(want_d))
+    assert np.array_equal(bi, want_i) and np.array_equal(_bits(bd), _bits(want_d))
+
+
+@pytest.mark.parametrize("dim,patch,ch", [(64, (8, 8), 1), (192, (8, 8), 3)])
+def test_exact_tc_ties_and_overflow(R, oracle_mod, dim, patch, ch):
+    """Duplicate references (ties -> lowest index, numpy argmin) and clusters of
+    near-identical references that overflow the screen's candidate list (those
+    queries take the exact full scan)."""
+    rng = np.random.default_rng(11)
+    base, _ = R.normalize_rows(rng.standard_normal((8, dim)).astype(np.float32))
+    near = np.repeat(base, 40, axis=0) + rng.standard_normal((320, dim)).astype(np.float32) * 1e-6
+    dup = np.repeat(base[:4], 3, axis=0)
+    refs = np.concatenate([near, dup, rng.standard_normal((200, dim)).astype(np.float32)])
+    refs, _ = R.normalize_rows(refs)
+    q = np.concatenate([base, refs[::7], rng.standard_normal((300, dim)).astype(np.float32) * 0.1])
+    q = np.ascontiguousarray(q, np.float32)
+    model = R.ReferenceModel.from_refs(refs, patch, channels=ch)
+    want_i, want_d = oracle_mod.exact_nn_batch(refs, q)
+    gi, gd, checked, fb = _exact_stats(model, q)
+    assert np.array_equal(gi, want_i) and np.array_equal(_bits(gd), _bits(want_d))
+    assert fb >= 8, "near-identical clusters should overflow the candidate list"
+    (ai, ad), (bi, bd) = _exact_both_paths(R, q, model)
+    assert np.array_equal(ai, want_i) and np.array_equal(bi, want_i)
+
+
+def test_exact_tc_field_cfg3_sample(R):
+    """Config-3 shape (D=192, n=8192 here): the tensor-core path and the SIMT
+    scan agree bit for bit on 20,000 frame units; the screen re-checks only a
+    few candidates per query."""
+    from dataclasses import replace
+
+    from paper_1508_07953_b200 import workloads as W
+
+    cfg = replace(W.CONFIGS[3], height=120, width=200, frames=1, n_refs=8192)
+    frame = W.clip(cfg, 1)[0]
+    refs = W.reference_set(cfg)
+    model = R.ReferenceModel.from_refs(refs, cfg.patch, channels=cfg.channels)
+    units = R.frame_units(frame, model)[:20000]
+    (ai, ad), (bi, bd) = _exact_both_paths(R, units, model)
+    assert np.array_equal(ai, bi) and np.array_equal(_bits(ad), _bits(bd))
+    _, _, checked, fb = _exact_stats(model, units)
+    assert checked < 8 * len(units) and fb < len(units) // 100

@@ -159,7 +159,8 @@ class Context:
         h = C.c_void_p()
         check(lib().riann_ctx_create(int(device), C.byref(h)))
         self.h = h
-        self.model_token = None    # object identity of the resident model
+        self.model_token = None    # object identity of the resident model (refs + sorted tables)
+        self.refs_token = None     # object identity of the model whose refs are resident
         self.field_gen = 0         # generation of the device-resident field
         self.units_gen = 0         # generation of the device-resident prev units
         self.lock = threading.RLock()

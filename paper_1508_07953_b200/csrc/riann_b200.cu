@@ -190,7 +190,7 @@ struct riann_ctx {
     bool bulk_disabled = false;
     // K4 tensor-core comparator: split reference operand, norms, per-call scratch
     bool exact_simt = false, x_ready = false;
-    DevBuf x_B, x_nr, x_center, x_A, x_nq, x_cand, x_lb, x_ncand, x_ub, x_fb, x_q, x_idx, x_dist;
+    DevBuf x_B, x_nr, x_center, x_scal, x_A, x_nq, x_cand, x_lb, x_ncand, x_ub, x_fb, x_q, x_idx, x_dist;
     uint64_t x_checked = 0, x_fallback = 0;
     // bulk-path frame buffers
     DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_grouped,
@@ -824,7 +824,7 @@ int riann_ctx_destroy(riann_ctx *c)
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
                       &c->q_cand, &c->q_first, &c->q_scanned, &c->q_scanned_len, &c->small,
                       &c->tree.leaf_start, &c->tree.leaf_len, &c->tree.leaf_node, &c->tree.level_off,
-                      &c->tree.inner, &c->tree.left, &c->tree.right, &c->tree.node_val, &c->x_B, &c->x_nr, &c->x_center,
+                      &c->tree.inner, &c->tree.left, &c->tree.right, &c->tree.node_val, &c->x_B, &c->x_nr, &c->x_center, &c->x_scal,
                       &c->x_A, &c->x_nq, &c->x_cand, &c->x_lb, &c->x_ncand, &c->x_ub, &c->x_fb, &c->x_q,
                       &c->x_idx, &c->x_dist};
     for (DevBuf *b : bufs) b->release();
@@ -1520,8 +1520,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// 2-D bf16 operand (rows, kcols), K-major, 64 x 128 boxes with the 128-byte swizzle
-int encode_operand(CUtensorMap *map, const void *base, int64_t rows, int kcols)
+// 2-D fp16 operand (rows, kcols), K-major, 64 x box_rows boxes with the 128-byte swizzle
+int encode_operand(CUtensorMap *map, const void *base, int64_t rows, int kcols, int box_rows)
 {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
@@ -1533,22 +1533,28 @@ int encode_operand(CUtensorMap *map, const void *base, int64_t rows, int kcols)
     }
     cuuint64_t dims[2] = {(cuuint64_t)kcols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)kcols * 2};
-    cuuint32_t box[2] = {(cuuint32_t)rb::tc::BK, (cuuint32_t)rb::tc::BM};
+    cuuint32_t box[2] = {(cuuint32_t)rb::tc::BK, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(RIANN_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return 0;
 }
 
-// |d2_est - d2| <= E * (||q||^2 + ||r||^2) for the 3-term bf16 split with K = 3D:
-//   split residual   <= 3.1 * 2^-16 * ||q|| ||r||
-//   fp32 accumulation <= 2K * 2^-23 * 1.02 ||q|| ||r||  (4x the round-to-nearest gamma_K, for truncating adders)
-//   norms + d2 arithmetic in float <= 8 * 2^-24 * (||q||^2 + ||r||^2)
-//   centring rounding (|fl(x-c) - (x-c)| <= 2^-24 |fl(x-c)|) <= 5 * 2^-24 * (||q||^2 + ||r||^2)
-// with q, r the centred rows, and 2 ||q|| ||r|| <= ||q||^2 + ||r||^2.  Rounded up generously.
-float exact_eps(int K) { return (float)(4.0 * std::ldexp(1.0, -16) + 2.1 * K * std::ldexp(1.0, -23) + std::ldexp(1.0, -19)); }
+// Relative screen error E: |d2_est - d^2| <= E (||q'||^2 + ||r'||^2) + E_abs with q', r' the
+// centred rows (exact_scal_kernel computes E_abs):
+//   fp16 operand rounding (unit roundoff u = 2^-11, normal range after the power-of-two
+//     scaling):  |q^.r^ - q.r| <= (2u + u^2) ||q|| ||r||, doubled for d^2
+//   fp32 accumulation of K = D exact products: 2K * 2^-23 * sum|q_i r_i| (4x the
+//     round-to-nearest gamma_K, for adders that truncate), doubled for d^2
+//   centring, norm rounding and the float arithmetic of the bounds: < 64 * 2^-24
+// using 2 ||q|| ||r|| <= ||q||^2 + ||r||^2.
+float exact_eps(int K)
+{
+    const double u = std::ldexp(1.0, -11);
+    return (float)((2 * u + u * u) * 1.01 + 2.1 * K * std::ldexp(1.0, -23) + 64 * std::ldexp(1.0, -24));
+}
 
 // fallback list (m int32) then the counters [fallbacks i32, pad, checked u64], 16-byte aligned
 size_t fb_counters_off(int64_t m) { return ((size_t)m * 4 + 15) & ~(size_t)15; }
@@ -1559,51 +1565,69 @@ template <int D>
 int exact_tc_run(riann_ctx *c, const float *dq, int64_t m, int32_t *didx, double *ddist)
 {
     namespace T = rb::tc;
-    constexpr int K = 3 * D;
+    constexpr int KB = D / T::BK;
     const int64_t n = c->n;
     const unsigned eblocks = (unsigned)c->sms * 8;
+    const float E = exact_eps(D);
+    // x_center: [center f32 x D | pad to 8 | acc f64 x D]; x_scal: [Scal | maxr u32 | maxq u32]
+    RET(c->x_scal.ensure(64));
+    T::Scal *scal = c->x_scal.as<T::Scal>();
+    unsigned *maxr = reinterpret_cast<unsigned *>(c->x_scal.as<char>() + 16);
+    unsigned *maxq = maxr + 1;
+    const float *center = c->x_center.as<float>();
     if (!c->x_ready) {
-        RET(c->x_B.ensure((size_t)n * K * 2));
-        RET(c->x_nr.ensure((size_t)n * 4));
-        RET(c->x_center.ensure((size_t)D * 12));
-        double *cacc = reinterpret_cast<double *>(c->x_center.as<char>() + (size_t)D * 4);
+        RET(c->x_B.ensure((size_t)n * D * 2));
+        RET(c->x_nr.ensure((size_t)n * 8 + ((size_t)(n + 31) / 32) * 4));
+        RET(c->x_center.ensure((size_t)D * 16 + 16));
+        center = c->x_center.as<float>();
+        double *cacc = reinterpret_cast<double *>(c->x_center.as<char>() + (((size_t)D * 4 + 15) & ~(size_t)15));
         CK(cudaMemsetAsync(cacc, 0, (size_t)D * 8, c->stream));
+        CK(cudaMemsetAsync(maxr, 0, 4, c->stream));
         T::center_sum_kernel<<<(unsigned)((n + 1023) / 1024), D, 0, c->stream>>>(c->refs.as<float>(), n, D, cacc);
         T::center_fin_kernel<<<1, D, 0, c->stream>>>(cacc, n, D, c->x_center.as<float>());
-        T::split_kernel<<<eblocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->x_center.as<float>(), n, D, 0,
-                                                        c->x_B.as<__nv_bfloat16>());
-        T::norm2_kernel<<<eblocks, 256, 0, c->stream>>>(c->refs.as<float>(), c->x_center.as<float>(), n, D,
-                                                        c->x_nr.as<float>());
+        T::absmax_kernel<<<eblocks, 256, 0, c->stream>>>(c->refs.as<float>(), center, n, D, maxr);
+        T::split_kernel<<<eblocks, 256, 0, c->stream>>>(c->refs.as<float>(), center, n, D, maxr,
+                                                        c->x_B.as<__half>());
+        T::norm2_kernel<<<eblocks, 256, 0, c->stream>>>(c->refs.as<float>(), center, n, D, E, nullptr,
+                                                        c->x_nr.as<float>(), c->x_nr.as<float>() + n);
+        T::chunk_slack_kernel<<<eblocks, 256, 0, c->stream>>>(c->x_nr.as<float>(), c->x_nr.as<float>() + n, n,
+                                                              c->x_nr.as<float>() + 2 * n);
         CK(cudaGetLastError());
         c->x_ready = true;
     }
-    RET(c->x_A.ensure((size_t)m * K * 2));
+    RET(c->x_A.ensure((size_t)m * D * 2));
     RET(c->x_nq.ensure((size_t)m * 4));
-    RET(c->x_cand.ensure((size_t)m * T::NCAND * 4));
-    RET(c->x_lb.ensure((size_t)m * T::NCAND * 4));
-    RET(c->x_ncand.ensure((size_t)m * 4));
-    RET(c->x_ub.ensure((size_t)m * 4));
+    RET(c->x_cand.ensure((size_t)m * 2 * T::NCAND * 4));
+    RET(c->x_lb.ensure((size_t)m * 2 * T::NCAND * 4));
+    RET(c->x_ncand.ensure((size_t)m * 8));
+    RET(c->x_ub.ensure((size_t)m * 8));
     RET(c->x_fb.ensure(fb_counters_off(m) + 64));
-    T::split_kernel<<<eblocks, 256, 0, c->stream>>>(dq, c->x_center.as<float>(), m, D, 1, c->x_A.as<__nv_bfloat16>());
-    T::norm2_kernel<<<eblocks, 256, 0, c->stream>>>(dq, c->x_center.as<float>(), m, D, c->x_nq.as<float>());
+    CK(cudaMemsetAsync(maxq, 0, 4, c->stream));
+    T::absmax_kernel<<<eblocks, 256, 0, c->stream>>>(dq, center, m, D, maxq);
+    T::split_kernel<<<eblocks, 256, 0, c->stream>>>(dq, center, m, D, maxq, c->x_A.as<__half>());
+    T::norm2_kernel<<<eblocks, 256, 0, c->stream>>>(dq, center, m, D, E, c->x_nq.as<float>(), nullptr, nullptr);
+    T::exact_scal_kernel<<<1, 1, 0, c->stream>>>(maxq, maxr, D, E, scal);
     CK(cudaGetLastError());
     CUtensorMap mapA, mapB;
-    RET(encode_operand(&mapA, c->x_A.p, m, K));
-    RET(encode_operand(&mapB, c->x_B.p, n, K));
+    RET(encode_operand(&mapA, c->x_A.p, m, D, T::BM));
+    RET(encode_operand(&mapB, c->x_B.p, n, D, T::BN));
     T::ExactParams P{};
     P.nq = c->x_nq.as<float>();
-    P.nr = c->x_nr.as<float>();
+    P.nrU = c->x_nr.as<float>();
+    P.nrL = c->x_nr.as<float>() + n;
+    P.dlt = c->x_nr.as<float>() + 2 * n;
+    P.scal = scal;
     P.m = m;
     P.n = n;
-    P.kblocks = K / T::BK;
-    P.eps = exact_eps(K);
+    P.kblocks = KB;
+    P.stages = T::stages_for(KB);
     P.cand = c->x_cand.as<int32_t>();
     P.cand_lb = c->x_lb.as<float>();
     P.ncand = c->x_ncand.as<int32_t>();
     P.best_ub = c->x_ub.as<float>();
-    const int smem = T::smem_bytes(P.kblocks);
+    const int smem = T::smem_bytes(KB);
     CK(cudaFuncSetAttribute(T::exact_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    T::exact_tc_kernel<<<(unsigned)((m + T::BM - 1) / T::BM), 256, smem, c->stream>>>(mapA, mapB, P);
+    T::exact_tc_kernel<<<(unsigned)((m + T::BM - 1) / T::BM), T::THREADS, smem, c->stream>>>(mapA, mapB, P);
     CK(cudaGetLastError());
     int32_t *nfb = reinterpret_cast<int32_t *>(c->x_fb.as<char>() + fb_counters_off(m));
     unsigned long long *nchk = reinterpret_cast<unsigned long long *>(c->x_fb.as<char>() + fb_counters_off(m) + 8);
@@ -1615,7 +1639,7 @@ int exact_tc_run(riann_ctx *c, const float *dq, int64_t m, int32_t *didx, double
     T::exact_list_kernel<D><<<(unsigned)c->sms * 8, 256, 0, c->stream>>>(c->refs.as<float>(), n, dq,
                                                                          c->x_fb.as<int32_t>(), nfb, didx, ddist);
     CK(cudaGetLastError());
-    c->launches += 5;
+    c->launches += 8;
     return 0;
 }
 
@@ -1684,10 +1708,25 @@ int riann_exact_field(riann_ctx *c, const float *frame, int H, int W, int C, int
 {
     RET(check_model(c, false));
     RET(check_frame(c, H, W, C));
+    RET(c->use());
     const int64_t Q = (int64_t)(W - c->pw + 1) * (H - c->ph + 1);
-    std::vector<float> unit((size_t)Q * c->dim);
-    RET(riann_frame_units(c, frame, H, W, C, unit.data(), nullptr));
-    return riann_exact_nn_batch(c, unit.data(), Q, out_idx, out_dist);
+    const size_t fbytes = (size_t)H * W * C * 4;
+    RET(c->frame.ensure(fbytes));
+    CK(cudaMemcpyAsync(c->frame.p, frame, fbytes, cudaMemcpyHostToDevice, c->stream));
+    RET(c->x_q.ensure((size_t)Q * c->dim * 4));
+    RET(c->x_idx.ensure((size_t)Q * 4));
+    RET(c->x_dist.ensure((size_t)Q * 8));
+    RET(launch_units(c, c->frame.as<float>(), H, W, C, c->x_q.as<float>(), nullptr, nullptr, nullptr));
+    // bounded launches (config 4: 8.25 M queries x 262,144 references)
+    const int64_t chunk = (int64_t)1 << 20;
+    for (int64_t q0 = 0; q0 < Q; q0 += chunk) {
+        const int64_t m = std::min(chunk, Q - q0);
+        RET(exact_run(c, c->x_q.as<float>() + q0 * c->dim, m, c->x_idx.as<int32_t>() + q0, c->x_dist.as<double>() + q0));
+    }
+    CK(cudaMemcpyAsync(out_idx, c->x_idx.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(out_dist, c->x_dist.p, (size_t)Q * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
 }
 
 int riann_init_field(int gw, int gh, int64_t n, const uint32_t *seed_words, int nwords, int32_t *out)

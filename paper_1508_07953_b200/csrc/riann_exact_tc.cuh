@@ -2,50 +2,79 @@
 // the distance screen on the 5th-generation tensor cores.
 //
 //   ||q - r||^2 = ||q'||^2 + ||r'||^2 - 2 q'.r' on operands centred on the
-//   reference mean (q' = q - c, r' = r - c), with q'.r' from one tcgen05 GEMM
-//   over K = 3D bf16 columns: A = [q'_hi, q'_hi, q'_lo], B = [r'_hi, r'_lo,
-//   r'_hi] (x_hi = bf16(x), x_lo = bf16(x - x_hi)), fp32 accumulation in TMEM.
+//   reference mean (q' = q - c, r' = r - c; distances are translation
+//   invariant and the screen's error then scales with the patch spread), with
+//   q'.r' from one tcgen05 GEMM (kind::f16, fp16 operands scaled by powers of
+//   two into fp16's normal range, fp32 accumulation in TMEM), K = D.
 //
-// Warp roles per CTA (one 128-query M tile, all N tiles of 128 references):
-//   warp 0  TMA producer (A and B K-blocks, 128B swizzle, 4-stage ring)
-//   warp 1  MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M=128 N=128 K=16)
-//   warp 2  TMEM allocator
-//   warps 4-7 epilogue: tcgen05.ld of the accumulator (double-buffered in
-//           TMEM), rigorous bounds, per-query running best upper bound and a
-//           short list of candidates whose lower bound can still reach it.
-// A second kernel re-evaluates the candidates with the exact float64 distance
-// in numpy's order (first minimum, lowest index on ties); queries whose list
-// overflowed take the exact full scan.  The screen only decides which
-// candidates get the exact distance, so results are bit-identical.
+//   Rigorous screen: |d2_est - d^2| <= E (||q'||^2 + ||r'||^2) + E_abs
+//   (exact_eps, riann_b200.cu).  Each query keeps the smallest upper bound
+//   u2 = d2_est + err and every reference whose lower bound l2 = d2_est - err
+//   does not exceed it; the exact nearest reference always survives.
+//
+// Warp roles per CTA (one 128-query M tile resident in shared memory, all
+// N tiles of 256 references streamed):
+//   warp 0     TMA producer (query tile once; reference K-blocks through a
+//              STAGES-deep ring, 128B swizzle)
+//   warp 1     MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16)
+//   warp 2     TMEM allocator (2 x 256 fp32 accumulator columns)
+//   warps 4-11 epilogue: warp w reads TMEM lane quarter w%4 and column half
+//              (w-4)/4 of the double-buffered accumulator (tcgen05.ld), two
+//              FFMAs and a min per element, a short candidate list per
+//              (query, half).
+// exact_recheck_kernel re-evaluates the survivors with the exact float64
+// distance in numpy's order (first minimum, lowest index on ties); queries
+// whose list overflowed take the exact full scan (exact_list_kernel).  The
+// screen only decides which references get the exact distance, so results
+// are bit-identical to exact_nn.
 #pragma once
 
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "riann_kernels.cuh"
 
 namespace rb {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 64;  // BK bf16 = 128 bytes per row (one swizzle atom)
-constexpr int STAGES = 4;
+constexpr int BM = 128, BN = 256, BK = 64;       // BK fp16 = 128 bytes per row (one swizzle atom)
 constexpr int A_BLOCK = BM * BK * 2;             // 16 KB: one K-block of the resident query tile
-constexpr int STAGE_BYTES = BN * BK * 2;         // 16 KB: one K-block of a reference tile
-constexpr int MAX_KB = 9;                        // 3D / BK for D = 192
-__host__ __device__ constexpr int smem_bytes(int kb) { return kb * A_BLOCK + STAGES * STAGE_BYTES + 1024; }
-constexpr int NCAND = 16;                      // candidates kept per query
-constexpr int EPI_WARP0 = 4;
+constexpr int STAGE_BYTES = BN * BK * 2;         // 32 KB: one K-block of a reference tile
+constexpr int NCAND = 16;                        // candidates kept per (query, column half)
+constexpr int EPI_WARP0 = 4, EPI_WARPS = 8;
+constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
+constexpr int HALF = BN / 2;                     // columns per epilogue warp
+constexpr int NRBUF = EPI_WARPS * 2 * HALF * 4;  // per-warp staged (1+E)nr, (1-E)nr
+constexpr int SMEM_LIMIT = 227 * 1024;
+__host__ __device__ constexpr int stages_for(int kb)
+{
+    return (SMEM_LIMIT - 1024 - NRBUF - kb * A_BLOCK) / STAGE_BYTES > 6
+               ? 6
+               : (SMEM_LIMIT - 1024 - NRBUF - kb * A_BLOCK) / STAGE_BYTES;
+}
+__host__ __device__ constexpr int smem_bytes(int kb) { return 1024 + kb * A_BLOCK + stages_for(kb) * STAGE_BYTES + NRBUF; }
+
+// device-side scalars of one call (exact_scal_kernel)
+struct Scal {
+    float coef;   // -2 * 2^-(Sa + Sb): fp32 accumulator -> -2 q'.r'
+    float eabs;   // absolute error term
+    float E;      // relative error factor
+    float pad;
+};
 
 struct ExactParams {
-    const float *nq;       // (m) ||q - c||^2 (float64 sum rounded to float)
-    const float *nr;       // (n) ||r - c||^2
+    const float *nq;       // (m) ||q'||^2 (float64 sum rounded to float)
+    const float *nrU;      // (n) (1+E) ||r'||^2, rounded up
+    const float *nrL;      // (n) (1-E) ||r'||^2, rounded down
+    const float *dlt;      // (ceil(n/32)) per 32-column chunk: max (nrU - nrL) + 2^-21 max nrU, rounded up
+    const Scal *scal;
     int64_t m, n;
-    int kblocks;           // 3D / BK
-    float eps;             // |d2_est - d2| <= eps * (nq + nr)  (see exact_eps)
-    int32_t *cand;         // (m, NCAND)
-    float *cand_lb;        // (m, NCAND)
-    int32_t *ncand;        // (m): count, or -1 on overflow
-    float *best_ub;        // (m)
+    int kblocks;           // D / BK
+    int stages;
+    int32_t *cand;         // (m, 2, NCAND)
+    float *cand_lb;        // (m, 2, NCAND) lower bounds (squared)
+    int32_t *ncand;        // (m, 2): count, or -1 on overflow
+    float *best_ub;        // (m, 2) smallest upper bound (squared)
 };
 
 __device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -95,17 +124,15 @@ __device__ __forceinline__ uint64_t smem_desc(const void *p)
     return d;
 }
 
-// kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major
+// kind::f16 instruction descriptor: F16 x F16 -> F32 (A/B format 0 = F16), both K-major
 __host__ __device__ constexpr uint32_t instr_desc(int M, int N)
 {
     return (1u << 4)                      // D format F32
-           | (1u << 7)                    // A format BF16
-           | (1u << 10)                   // B format BF16
            | ((uint32_t)(N >> 3) << 17)   // N / 8
            | ((uint32_t)(M >> 4) << 24);  // M / 16
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc)
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc)
 {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -133,26 +160,31 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(256, 1) exact_tc_kernel(const __grid_constant__ CUtensorMap mapA,
-                                                           const __grid_constant__ CUtensorMap mapB, ExactParams P)
+__global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_constant__ CUtensorMap mapA,
+                                                               const __grid_constant__ CUtensorMap mapB, ExactParams P)
 {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], acc_full[2], acc_empty[2], a_bar;
+    // 1024-byte alignment for the 128B swizzle, by pointer arithmetic so accesses stay ld.shared
+    unsigned char *smem = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
+    constexpr int MAXST = 8;
+    __shared__ uint64_t full_bar[MAXST], empty_bar[MAXST], acc_full[2], acc_empty[2], a_bar;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t m0 = (int64_t)blockIdx.x * BM;
     const int ntiles = (int)((P.n + BN - 1) / BN);
-    const int kb = P.kblocks;
+    const int kb = P.kblocks, ST = P.stages;
+    unsigned char *sA = smem;                         // kb resident K-blocks of the query tile
+    unsigned char *sB = smem + kb * A_BLOCK;          // ST reference K-blocks
+    float *sNr = reinterpret_cast<float *>(sB + ST * STAGE_BYTES);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; s++) {
+        for (int s = 0; s < ST; s++) {
             bar_init(&full_bar[s], 1);
             bar_init(&empty_bar[s], 1);
         }
         for (int a = 0; a < 2; a++) {
             bar_init(&acc_full[a], 1);
-            bar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
+            bar_init(&acc_empty[a], EPI_WARPS);  // one arrive per epilogue warp
         }
         bar_init(&a_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -167,8 +199,6 @@ __global__ void __launch_bounds__(256, 1) exact_tc_kernel(const __grid_constant_
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = tmem_base;
 
-    unsigned char *sA = smem;                    // kb resident K-blocks of the query tile
-    unsigned char *sB = smem + kb * A_BLOCK;     // STAGES reference K-blocks
     if (warp == 0) {
         // ---- TMA producer
         if (lane == 0) {
@@ -177,8 +207,8 @@ __global__ void __launch_bounds__(256, 1) exact_tc_kernel(const __grid_constant_
             int it = 0;
             for (int t = 0; t < ntiles; t++) {
                 for (int k = 0; k < kb; k++, it++) {
-                    const int s = it % STAGES;
-                    if (it >= STAGES) bar_wait(&empty_bar[s], (unsigned)(((it / STAGES) - 1) & 1));
+                    const int s = it % ST;
+                    if (it >= ST) bar_wait(&empty_bar[s], (unsigned)(((it / ST) - 1) & 1));
                     bar_expect(&full_bar[s], STAGE_BYTES);
                     tma_load_2d(sB + s * STAGE_BYTES, &mapB, k * BK, t * BN, &full_bar[s]);
                 }
@@ -195,14 +225,14 @@ __global__ void __launch_bounds__(256, 1) exact_tc_kernel(const __grid_constant_
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t tacc = tbase + (uint32_t)(acc * BN);
             for (int k = 0; k < kb; k++, it++) {
-                const int s = it % STAGES;
-                bar_wait(&full_bar[s], (unsigned)((it / STAGES) & 1));
+                const int s = it % ST;
+                bar_wait(&full_bar[s], (unsigned)((it / ST) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
                     const uint64_t da = smem_desc(sA + k * A_BLOCK), db = smem_desc(sB + s * STAGE_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; kk++)  // 16 bf16 = 32 bytes per MMA step
-                        mma_bf16(tacc, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc, (k | kk) ? 1u : 0u);
+                    for (int kk = 0; kk < BK / 16; kk++)  // 16 fp16 = 32 bytes per MMA step
+                        mma_f16(tacc, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc, (k | kk) ? 1u : 0u);
                     mma_commit(&empty_bar[s]);
                     if (k == kb - 1) mma_commit(&acc_full[acc]);
                 }
@@ -210,95 +240,132 @@ __global__ void __launch_bounds__(256, 1) exact_tc_kernel(const __grid_constant_
             }
         }
     } else if (warp >= EPI_WARP0) {
-        // ---- epilogue: thread owns query row r of the tile (TMEM lane r)
-        const int q4 = warp - EPI_WARP0;  // TMEM lane quarter
+        // ---- epilogue: thread owns query row r (TMEM lane r), columns [h*HALF, (h+1)*HALF) of each tile
+        const int ew = warp - EPI_WARP0;
+        const int q4 = ew & 3, h = ew >> 2;
         const int r = q4 * 32 + lane;
         const int64_t qi = m0 + r;
         const bool rowok = qi < P.m;
+        const Scal sc = *P.scal;
         const float nq = rowok ? P.nq[qi] : 0.f;
-        // squared-distance space: u2 >= d^2 >= l2 for every reference
-        float ub2 = __int_as_float(0x7f800000);
-        int cnt = 0;
+        const float cu = __fadd_ru(__fmul_ru(__fadd_ru(1.f, sc.E), nq), sc.eabs);  // u2 = cu + w
+        const float cl0 = __fsub_rd(__fmul_rd(__fsub_rd(1.f, sc.E), nq), sc.eabs);  // l2 = cl0 + v
+        const float coef = sc.coef;
+        const float inf = __int_as_float(0x7f800000);
+        float ub2 = inf;
+        int cnt = rowok ? 0 : -2;
         int32_t cj[NCAND];
         float cl[NCAND];
-        const float inf = __int_as_float(0x7f800000);
-        // nr of the tile's 128 columns, 4 per lane (column c0 + x lives in lane x of nrv[c0 / 32])
-        float nrv[BN / 32], nrn[BN / 32];
+        float *myU = sNr + ew * 2 * HALF, *myL = myU + HALF;
+        const float sq = __fmul_ru(nq, 4.76837158203125e-7f);  // 2^-21 nq: rounding slack of w and v
+        // (1+E)nr / (1-E)nr of this warp's columns, 4 per lane, and the chunk slack dlt (lane k < 4 holds
+        // chunk k), prefetched one tile ahead
+        float pu[HALF / 32], pl[HALF / 32], pd;
+        const int64_t nchunks = (P.n + 31) / 32;
 #pragma unroll
-        for (int k = 0; k < BN / 32; k++) {
-            const int64_t j = (int64_t)k * 32 + lane;
-            nrv[k] = j < P.n ? __ldg(P.nr + j) : inf;
+        for (int k = 0; k < HALF / 32; k++) {
+            const int64_t j = (int64_t)h * HALF + k * 32 + lane;
+            pu[k] = j < P.n ? __ldg(P.nrU + j) : inf;
+            pl[k] = j < P.n ? __ldg(P.nrL + j) : inf;
+        }
+        {
+            const int64_t ch = (int64_t)h * (HALF / 32) + (lane & 3);
+            pd = ch < nchunks ? __ldg(P.dlt + ch) : 0.f;
         }
         for (int t = 0; t < ntiles; t++) {
             const int acc = t & 1;
+            __syncwarp();
 #pragma unroll
-            for (int k = 0; k < BN / 32; k++) {  // prefetch the next tile's norms
-                const int64_t j = (int64_t)(t + 1) * BN + k * 32 + lane;
-                nrn[k] = j < P.n ? __ldg(P.nr + j) : inf;
+            for (int k = 0; k < HALF / 32; k++) {
+                myU[k * 32 + lane] = pu[k];
+                myL[k * 32 + lane] = pl[k];
+            }
+            __syncwarp();
+            const float dcur = pd;
+#pragma unroll
+            for (int k = 0; k < HALF / 32; k++) {
+                const int64_t j = (int64_t)(t + 1) * BN + h * HALF + k * 32 + lane;
+                pu[k] = j < P.n ? __ldg(P.nrU + j) : inf;
+                pl[k] = j < P.n ? __ldg(P.nrL + j) : inf;
+            }
+            {
+                const int64_t ch = ((int64_t)(t + 1) * BN + h * HALF) / 32 + (lane & 3);
+                pd = ch < nchunks ? __ldg(P.dlt + ch) : 0.f;
             }
             bar_wait(&acc_full[acc], (unsigned)((t / 2) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int k = 0; k < HALF / 32; k++) {
+                uint32_t acc32[32];
+                tmem_ld32(tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN + h * HALF + k * 32), acc32);
+                // fast path: w = coef*dot + (1+E)nr; u2 = cu + w is an upper bound of d^2
+                float wmin = inf;
 #pragma unroll
-            for (int k = 0; k < BN / 32; k++) {
-                uint32_t v[32];
-                tmem_ld32(tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN + k * 32), v);
-                float d2[32], e[32];
-                float cmin = inf;
-#pragma unroll
-                for (int x = 0; x < 32; x++) {
-                    const float s = __fadd_rn(nq, __shfl_sync(FULL, nrv[k], x));  // inf past n
-                    d2[x] = __fmaf_rn(-2.f, __uint_as_float(v[x]), s);
-                    e[x] = __fmul_ru(P.eps, s);
-                    cmin = fminf(cmin, __fadd_ru(d2[x], e[x]));
+                for (int x = 0; x < 32; x += 4) {
+                    const float4 u4 = *reinterpret_cast<const float4 *>(myU + k * 32 + x);
+                    wmin = fminf(wmin, fminf(fminf(__fmaf_rn(coef, __uint_as_float(acc32[x]), u4.x),
+                                                   __fmaf_rn(coef, __uint_as_float(acc32[x + 1]), u4.y)),
+                                             fminf(__fmaf_rn(coef, __uint_as_float(acc32[x + 2]), u4.z),
+                                                   __fmaf_rn(coef, __uint_as_float(acc32[x + 3]), u4.w))));
                 }
-                ub2 = fminf(ub2, cmin);
-                uint32_t mask = 0;
+                ub2 = fminf(ub2, __fadd_ru(cu, wmin));
+                const float thr = __fsub_ru(ub2, cl0);
+                // v = coef*dot + (1-E)nr >= w - dlt - sq, so no v <= thr unless wmin <= thr + dlt + sq
+                const float dk = __shfl_sync(FULL, dcur, k);
+                if (wmin <= __fadd_ru(__fadd_ru(thr, dk), sq) && cnt >= 0) {  // rare
+                    uint32_t mask = 0;
+                    float v[32];
 #pragma unroll
-                for (int x = 0; x < 32; x++) mask |= (__fsub_rd(d2[x], e[x]) <= ub2 ? 1u : 0u) << x;
-                if (!rowok) mask = 0;
-                while (mask && cnt >= 0) {  // rare: candidates that can still win
-                    const int x = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    float l2 = 0.f;
-#pragma unroll
-                    for (int y = 0; y < 32; y++)
-                        if (y == x) l2 = __fsub_rd(d2[y], e[y]);
-                    if (cnt == NCAND) {  // compact with the current bound
-                        int w2 = 0;
-#pragma unroll
-                        for (int y = 0; y < NCAND; y++)
-                            if (cl[y] <= ub2) {
-                                cj[w2] = cj[y];
-                                cl[w2] = cl[y];
-                                w2++;
-                            }
-                        cnt = w2 == NCAND ? -1 : w2;  // -1: overflow, exact full scan
+                    for (int x = 0; x < 32; x += 4) {
+                        const float4 l4 = *reinterpret_cast<const float4 *>(myL + k * 32 + x);
+                        v[x] = __fmaf_rn(coef, __uint_as_float(acc32[x]), l4.x);
+                        v[x + 1] = __fmaf_rn(coef, __uint_as_float(acc32[x + 1]), l4.y);
+                        v[x + 2] = __fmaf_rn(coef, __uint_as_float(acc32[x + 2]), l4.z);
+                        v[x + 3] = __fmaf_rn(coef, __uint_as_float(acc32[x + 3]), l4.w);
                     }
-                    if (cnt >= 0) {
-                        cj[cnt] = (int32_t)((int64_t)t * BN + k * 32 + x);
-                        cl[cnt] = l2;
+#pragma unroll
+                    for (int x = 0; x < 32; x++) mask |= (v[x] <= thr ? 1u : 0u) << x;
+                    while (mask && cnt >= 0) {
+                        const int x = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        float vx = 0.f;
+#pragma unroll
+                        for (int y = 0; y < 32; y++) vx = y == x ? v[y] : vx;
+                        if (cnt == NCAND) {  // compact with the current bound
+                            int w2 = 0;
+#pragma unroll
+                            for (int y = 0; y < NCAND; y++)
+                                if (cl[y] <= ub2) {
+                                    cj[w2] = cj[y];
+                                    cl[w2] = cl[y];
+                                    w2++;
+                                }
+                            cnt = w2 == NCAND ? -1 : w2;  // -1: overflow, exact full scan
+                            if (cnt < 0) break;
+                        }
+                        cj[cnt] = (int32_t)((int64_t)t * BN + h * HALF + k * 32 + x);
+                        cl[cnt] = __fadd_rd(cl0, vx);
                         cnt++;
                     }
                 }
             }
-#pragma unroll
-            for (int k = 0; k < BN / 32; k++) nrv[k] = nrn[k];
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) bar_arrive(&acc_empty[acc]);
         }
         if (rowok) {
+            const int64_t o = qi * 2 + h;
             int w2 = 0;
             if (cnt >= 0) {
                 for (int y = 0; y < cnt; y++)
                     if (cl[y] <= ub2) {
-                        P.cand[qi * NCAND + w2] = cj[y];
-                        P.cand_lb[qi * NCAND + w2] = cl[y];
+                        P.cand[o * NCAND + w2] = cj[y];
+                        P.cand_lb[o * NCAND + w2] = cl[y];
                         w2++;
                     }
             }
-            P.ncand[qi] = cnt >= 0 ? w2 : -1;
-            P.best_ub[qi] = ub2;
+            P.ncand[o] = cnt >= 0 ? w2 : -1;
+            P.best_ub[o] = ub2;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -306,16 +373,11 @@ __global__ void __launch_bounds__(256, 1) exact_tc_kernel(const __grid_constant_
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(2 * BN));
 }
 
-// Operands are centred on the reference mean c before the split: distances
-// are translation-invariant and the screen's error scales with |q-c| |r-c|
-// (the patch spread) instead of |q| |r|.  v = fl(x - c) differs from x - c by
-// at most 2^-24 |v| per component, which exact_eps covers.
-// A rows: [v_hi, v_hi, v_lo], B rows: [v_hi, v_lo, v_hi];
-// v_hi = bf16(v), v_lo = bf16(v - v_hi) (v - v_hi is exact in float).
+// ---- operand preparation ---------------------------------------------------
+// centre c = mean of the references (float64 sums, rounded to float)
 __global__ void center_sum_kernel(const float *__restrict__ x, int64_t rows, int dim, double *__restrict__ acc)
 {
-    // block: dim threads (<= 256) over a chunk of 1024 rows
-    const int e = threadIdx.x;
+    const int e = threadIdx.x;  // block: dim threads (<= 256) over a chunk of 1024 rows
     if (e >= dim) return;
     const int64_t r0 = (int64_t)blockIdx.x * 1024, r1 = min(rows, r0 + 1024);
     double s = 0.0;
@@ -329,27 +391,43 @@ __global__ void center_fin_kernel(const double *__restrict__ acc, int64_t rows, 
     if (e < dim) center[e] = (float)(acc[e] / (double)rows);
 }
 
-__global__ void split_kernel(const float *__restrict__ x, const float *__restrict__ center, int64_t rows, int dim,
-                             int a_side, __nv_bfloat16 *__restrict__ out)
+// max |fl(x - c)| (non-negative floats order like their bit patterns); warp per row
+__global__ void absmax_kernel(const float *__restrict__ x, const float *__restrict__ center, int64_t rows, int dim,
+                              unsigned *__restrict__ out)
 {
+    float mx = 0.f;
     const int64_t total = rows * dim;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / dim;
-        const int e = (int)(i - r * dim);
-        const float v = __fsub_rn(x[i], center[e]);
-        const __nv_bfloat16 h = __float2bfloat16_rn(v);
-        const __nv_bfloat16 l = __float2bfloat16_rn(__fsub_rn(v, __bfloat162float(h)));
-        __nv_bfloat16 *o = out + r * 3 * dim + e;
-        o[0] = h;
-        o[dim] = a_side ? h : l;
-        o[2 * dim] = a_side ? l : h;
-    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        mx = fmaxf(mx, fabsf(__fsub_rn(x[i], center[i % dim])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(mx));
 }
 
-// squared norms of the centred rows, float64 sum rounded to float (covered by
-// eps); warp per row
+// power-of-two exponent S with max * 2^S in [2^13, 2^14)
+__device__ __forceinline__ int scale_exp(unsigned maxbits)
+{
+    const float mx = __uint_as_float(maxbits);
+    if (!(mx > 0.f)) return 0;
+    int ex;
+    frexpf(mx, &ex);  // mx = f * 2^ex, f in [0.5, 1)
+    return 14 - ex;
+}
+
+// fp16 operand rows: fl16(fl(x - c) * 2^S)
+__global__ void split_kernel(const float *__restrict__ x, const float *__restrict__ center, int64_t rows, int dim,
+                             const unsigned *__restrict__ maxbits, __half *__restrict__ out)
+{
+    const int S = scale_exp(*maxbits);
+    const int64_t total = rows * dim;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __float2half_rn(ldexpf(__fsub_rn(x[i], center[i % dim]), S));
+}
+
+// ||fl(x - c)||^2 (float64 sum rounded to float, covered by E); with E given,
+// also (1+E) n rounded up and (1-E) n rounded down.  Warp per row.
 __global__ void norm2_kernel(const float *__restrict__ x, const float *__restrict__ center, int64_t rows, int dim,
-                             float *__restrict__ norm2)
+                             float E, float *__restrict__ norm2, float *__restrict__ nU, float *__restrict__ nL)
 {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -362,8 +440,54 @@ __global__ void norm2_kernel(const float *__restrict__ x, const float *__restric
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(FULL, s, o));
-        if (lane == 0) norm2[r] = (float)s;
+        if (lane == 0) {
+            const float n2 = (float)s;
+            if (norm2) norm2[r] = n2;
+            if (nU) nU[r] = __fmul_ru(__fadd_ru(1.f, E), __double2float_ru(s));
+            if (nL) nL[r] = __fmul_rd(__fsub_rd(1.f, E), __double2float_rd(s));
+        }
     }
+}
+
+// per 32-column chunk: max (nrU - nrL) + 2^-21 max nrU, rounded up (fast-path slack); warp per chunk
+__global__ void chunk_slack_kernel(const float *__restrict__ nU, const float *__restrict__ nL, int64_t n,
+                                   float *__restrict__ dlt)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = w0; c < (n + 31) / 32; c += nw) {
+        const int64_t j = c * 32 + lane;
+        float d = 0.f, u = 0.f;
+        if (j < n) {
+            d = __fsub_ru(nU[j], nL[j]);
+            u = nU[j];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            d = fmaxf(d, __shfl_xor_sync(FULL, d, o));
+            u = fmaxf(u, __shfl_xor_sync(FULL, u, o));
+        }
+        if (lane == 0) dlt[c] = __fadd_ru(d, __fmul_ru(u, 4.76837158203125e-7f));
+    }
+}
+
+// per-call scalars: coef = -2 * 2^-(Sa+Sb); eabs from the fp16 subnormal spacing
+__global__ void exact_scal_kernel(const unsigned *__restrict__ maxq, const unsigned *__restrict__ maxr, int dim,
+                                  float E, Scal *__restrict__ out)
+{
+    const int Sa = scale_exp(*maxq), Sb = scale_exp(*maxr);
+    Scal s;
+    s.coef = -2.f * ldexpf(1.f, -(Sa + Sb));
+    // |fl16(v 2^S) - v 2^S| <= 2^-25 absolute below fp16's normal range, i.e. <= 2^-25-S in
+    // original units (<= 2^-38 max|v|); dot error <= D (a_q maxr + a_r maxq) + D a_q a_r, doubled
+    // for d^2, with a 4x margin
+    const double mq = (double)__uint_as_float(*maxq), mr = (double)__uint_as_float(*maxr);
+    const double aq = ldexp(1.0, -25 - Sa), ar = ldexp(1.0, -25 - Sb);
+    s.eabs = (float)(8.0 * dim * (aq * mr + ar * mq + aq * ar) + 1e-30);
+    s.E = E;
+    s.pad = 0.f;
+    *out = s;
 }
 
 // exact re-check of the screened candidates (numpy-order float64 distance)
@@ -379,21 +503,23 @@ __global__ void __launch_bounds__(256) exact_recheck_kernel(const float *refs, i
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t g = gw; g < m; g += nw) {
-        const int c = ncand[g];
-        if (c < 0) {
+        const int c0 = ncand[2 * g], c1 = ncand[2 * g + 1];
+        if (c0 < 0 || c1 < 0) {
             if (lane == 0) fallback[atomicAdd(nfallback, 1)] = (int32_t)g;
             continue;
         }
-        const float ub = best_ub[g];
+        const float ub = fminf(best_ub[2 * g], best_ub[2 * g + 1]);
         const float *q = qs + g * D;
+        const int c = c0 + c1;
         int checked = 0;
         double bd = __longlong_as_double(0x7ff0000000000000LL);
         int bi = 0x7fffffff;
         for (int s0 = 0; s0 < c; s0 += NGX) {
             const int si = s0 + lane / GX;
-            const bool ok = si < c && cand_lb[g * NCAND + si] <= ub;
+            const int64_t slot = si < c0 ? 2 * g * NCAND + si : (2 * g + 1) * NCAND + (si - c0);
+            const bool ok = si < c && cand_lb[si < c ? slot : 0] <= ub;
             checked += __popc(__ballot_sync(FULL, ok)) / GX;
-            const int j = cand[g * NCAND + (si < c ? si : 0)];
+            const int j = ok ? cand[slot] : 0;
             const double dj = exact_dist<D>(refs, j, q, D, lane % GX);
             if (ok) argmin_merge(bd, bi, dj, j);
         }

@@ -14,23 +14,11 @@ import numpy as np
 from . import _native as N
 from .engine import AnnField, _frame_for
 from .errors import DimensionError
+from .model import resident_refs
 
 
 def _upload_refs(ctx, model):
-    tok = ctx.model_token
-    if tok is not None and tok() is model:
-        return
-    refs = np.ascontiguousarray(model.refs, dtype=np.float32)
-    n, dim = refs.shape
-    pw, ph = int(model.patch_size[0]), int(model.patch_size[1])
-    channels = int(getattr(model, "channels", 1))
-    if pw * ph * channels != dim:
-        pw, ph, channels = dim, 1, 1
-    # refs only; the resident-model token is cleared so a later table user re-uploads
-    ctx.model_token = None
-    ctx.field_gen += 1
-    N.check(N.lib().riann_model_set_refs(ctx.h, N.ptr(refs), n, dim, pw, ph, channels,
-                                         int(getattr(model, "metric_id", 0))))
+    resident_refs(ctx, model)
 
 
 def exact_nn(query, model) -> tuple[int, float]:
@@ -43,9 +31,7 @@ def exact_nn(query, model) -> tuple[int, float]:
     dist = np.empty(1, np.float64)
     ctx = N.context()
     with ctx.lock:
-        tok = ctx.model_token
-        if tok is None or tok() is not model:
-            _upload_refs(ctx, model)
+        _upload_refs(ctx, model)
         N.check(N.lib().riann_exact_nn_batch(ctx.h, N.ptr(q), 1, N.ptr(idx), N.ptr(dist)))
     return int(idx[0]), float(dist[0])
 
@@ -61,9 +47,7 @@ def exact_nn_batch(queries, model):
     if m:
         ctx = N.context()
         with ctx.lock:
-            tok = ctx.model_token
-            if tok is None or tok() is not model:
-                _upload_refs(ctx, model)
+            _upload_refs(ctx, model)
             N.check(N.lib().riann_exact_nn_batch(ctx.h, N.ptr(q), m, N.ptr(idx), N.ptr(dist)))
     return idx, dist
 
@@ -81,8 +65,6 @@ def field_exact_oracle(frame, model) -> AnnField:
     dist = np.empty((gh, gw), np.float64)
     ctx = N.context()
     with ctx.lock:
-        tok = ctx.model_token
-        if tok is None or tok() is not model:
-            _upload_refs(ctx, model)
+        _upload_refs(ctx, model)
         N.check(N.lib().riann_exact_field(ctx.h, N.ptr(f), H, W, Cn, N.ptr(idx), N.ptr(dist)))
     return AnnField(width=gw, height=gh, indices=idx, distances=dist)

@@ -113,6 +113,32 @@ class ReferenceModel:
         self._si = si
 
 
+def _upload_refs_only(ctx: N.Context, model) -> None:
+    refs = np.ascontiguousarray(model.refs, dtype=np.float32)
+    n, dim = refs.shape
+    pw, ph = int(model.patch_size[0]), int(model.patch_size[1])
+    channels = int(getattr(model, "channels", 1))
+    if pw * ph * channels != dim:
+        pw, ph, channels = dim, 1, 1
+    ctx.model_token = None
+    ctx.refs_token = None
+    N.check(N.lib().riann_model_set_refs(ctx.h, N.ptr(refs), n, dim, pw, ph, channels,
+                                         int(getattr(model, "metric_id", 0))))
+    ctx.refs_token = weakref.ref(model)
+    ctx.field_gen += 1
+    ctx.units_gen += 1
+
+
+def resident_refs(ctx: N.Context, model) -> None:
+    """Make ``model``'s reference rows resident on ``ctx`` without the sorted
+    tables (enough for frame units and the exact comparator; n x n tables do
+    not fit at config 4's n = 262,144)."""
+    for tok in (ctx.model_token, ctx.refs_token):
+        if tok is not None and tok() is model:
+            return
+    _upload_refs_only(ctx, model)
+
+
 def resident(ctx: N.Context, model) -> None:
     """Make ``model`` (this package's or the reference's ReferenceModel) the
     model resident on ``ctx``; no-op when it already is."""
@@ -129,6 +155,7 @@ def resident(ctx: N.Context, model) -> None:
         # still valid for query-only use, so keep dim and derive a flat patch
         pw, ph, channels = dim, 1, 1
     ctx.model_token = None
+    ctx.refs_token = None
     N.check(N.lib().riann_model_set_refs(ctx.h, N.ptr(refs), n, dim, pw, ph, channels, metric_id))
     own = isinstance(model, ReferenceModel)
     if own and model._sd is None:
@@ -143,6 +170,7 @@ def resident(ctx: N.Context, model) -> None:
             raise ValueError("sorted_dist values must be exactly representable in float32 (model.py:178-179)")
         N.check(N.lib().riann_model_set_tables(ctx.h, N.ptr(sd32), N.ptr(si)))
     ctx.model_token = weakref.ref(model)
+    ctx.refs_token = ctx.model_token
     ctx.field_gen += 1
     ctx.units_gen += 1
 

@@ -66,7 +66,7 @@ def main():
         _upload_refs(ctx, model)
         torch.cuda.synchronize()
         ms, checked, fb = run(ctx, q, idx, dist, a.reps)
-        flop = 2.0 * m * n * 3 * D
+        flop = 2.0 * m * n * D  # algorithmic: one D-term dot product per (query, reference)
         out.update(tc_ms=ms, tc_queries_per_s=m / ms * 1e3, tc_tflops=flop / ms / 1e9,
                    rechecks_per_query=checked / m, fallback_queries=fb)
         tc_idx = idx.cpu().numpy().copy()

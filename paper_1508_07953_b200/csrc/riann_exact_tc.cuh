@@ -59,8 +59,16 @@ struct Scal {
     float coef;   // -2 * 2^-(Sa + Sb): fp32 accumulator -> -2 q'.r'
     float eabs;   // absolute error term
     float E;      // relative error factor
-    float pad;
+    float hs;     // 2^(Sa + Sb - 1) = -1 / coef: squared distances in accumulator units
 };
+
+// w = nr' - acc with the -1 as an immediate (FFMA imm form: twice the 3-register issue rate)
+__device__ __forceinline__ float sub_acc(float acc, float nr)
+{
+    float r;
+    asm("fma.rn.f32 %0, %1, 0fBF800000, %2;" : "=f"(r) : "f"(acc), "f"(nr));
+    return r;
+}
 
 struct ExactParams {
     const float *nq;       // (m) ||q'||^2 (float64 sum rounded to float)
@@ -248,16 +256,18 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
         const bool rowok = qi < P.m;
         const Scal sc = *P.scal;
         const float nq = rowok ? P.nq[qi] : 0.f;
-        const float cu = __fadd_ru(__fmul_ru(__fadd_ru(1.f, sc.E), nq), sc.eabs);  // u2 = cu + w
-        const float cl0 = __fsub_rd(__fmul_rd(__fsub_rd(1.f, sc.E), nq), sc.eabs);  // l2 = cl0 + v
-        const float coef = sc.coef;
+        // all bounds in accumulator units (x hs, an exact power of two):
+        //   u2 = cu + (nrU - acc),  l2 = cl0 + (nrL - acc)
+        const float hs = sc.hs;
+        const float cu = __fmul_ru(__fadd_ru(__fmul_ru(__fadd_ru(1.f, sc.E), nq), sc.eabs), hs);
+        const float cl0 = __fmul_rd(__fsub_rd(__fmul_rd(__fsub_rd(1.f, sc.E), nq), sc.eabs), hs);
         const float inf = __int_as_float(0x7f800000);
         float ub2 = inf;
         int cnt = rowok ? 0 : -2;
         int32_t cj[NCAND];
         float cl[NCAND];
         float *myU = sNr + ew * 2 * HALF, *myL = myU + HALF;
-        const float sq = __fmul_ru(nq, 4.76837158203125e-7f);  // 2^-21 nq: rounding slack of w and v
+        const float sq = __fmul_ru(__fmul_ru(nq, 4.76837158203125e-7f), hs);  // 2^-21 nq: rounding slack of w, v
         // (1+E)nr / (1-E)nr of this warp's columns, 4 per lane, and the chunk slack dlt (lane k < 4 holds
         // chunk k), prefetched one tile ahead
         float pu[HALF / 32], pl[HALF / 32], pd;
@@ -277,11 +287,11 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < HALF / 32; k++) {
-                myU[k * 32 + lane] = pu[k];
-                myL[k * 32 + lane] = pl[k];
+                myU[k * 32 + lane] = pu[k] * hs;
+                myL[k * 32 + lane] = pl[k] * hs;
             }
             __syncwarp();
-            const float dcur = pd;
+            const float dcur = pd * hs;
 #pragma unroll
             for (int k = 0; k < HALF / 32; k++) {
                 const int64_t j = (int64_t)(t + 1) * BN + h * HALF + k * 32 + lane;
@@ -298,19 +308,19 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
             for (int k = 0; k < HALF / 32; k++) {
                 uint32_t acc32[32];
                 tmem_ld32(tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN + h * HALF + k * 32), acc32);
-                // fast path: w = coef*dot + (1+E)nr; u2 = cu + w is an upper bound of d^2
+                // fast path: w = (1+E)nr - acc; u2 = cu + w is an upper bound of d^2
                 float wmin = inf;
 #pragma unroll
                 for (int x = 0; x < 32; x += 4) {
                     const float4 u4 = *reinterpret_cast<const float4 *>(myU + k * 32 + x);
-                    wmin = fminf(wmin, fminf(fminf(__fmaf_rn(coef, __uint_as_float(acc32[x]), u4.x),
-                                                   __fmaf_rn(coef, __uint_as_float(acc32[x + 1]), u4.y)),
-                                             fminf(__fmaf_rn(coef, __uint_as_float(acc32[x + 2]), u4.z),
-                                                   __fmaf_rn(coef, __uint_as_float(acc32[x + 3]), u4.w))));
+                    wmin = fminf(wmin, fminf(fminf(sub_acc(__uint_as_float(acc32[x]), u4.x),
+                                                   sub_acc(__uint_as_float(acc32[x + 1]), u4.y)),
+                                             fminf(sub_acc(__uint_as_float(acc32[x + 2]), u4.z),
+                                                   sub_acc(__uint_as_float(acc32[x + 3]), u4.w))));
                 }
                 ub2 = fminf(ub2, __fadd_ru(cu, wmin));
                 const float thr = __fsub_ru(ub2, cl0);
-                // v = coef*dot + (1-E)nr >= w - dlt - sq, so no v <= thr unless wmin <= thr + dlt + sq
+                // v = (1-E)nr - acc >= w - dlt - sq, so no v <= thr unless wmin <= thr + dlt + sq
                 const float dk = __shfl_sync(FULL, dcur, k);
                 if (wmin <= __fadd_ru(__fadd_ru(thr, dk), sq) && cnt >= 0) {  // rare
                     uint32_t mask = 0;
@@ -318,10 +328,10 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
 #pragma unroll
                     for (int x = 0; x < 32; x += 4) {
                         const float4 l4 = *reinterpret_cast<const float4 *>(myL + k * 32 + x);
-                        v[x] = __fmaf_rn(coef, __uint_as_float(acc32[x]), l4.x);
-                        v[x + 1] = __fmaf_rn(coef, __uint_as_float(acc32[x + 1]), l4.y);
-                        v[x + 2] = __fmaf_rn(coef, __uint_as_float(acc32[x + 2]), l4.z);
-                        v[x + 3] = __fmaf_rn(coef, __uint_as_float(acc32[x + 3]), l4.w);
+                        v[x] = sub_acc(__uint_as_float(acc32[x]), l4.x);
+                        v[x + 1] = sub_acc(__uint_as_float(acc32[x + 1]), l4.y);
+                        v[x + 2] = sub_acc(__uint_as_float(acc32[x + 2]), l4.z);
+                        v[x + 3] = sub_acc(__uint_as_float(acc32[x + 3]), l4.w);
                     }
 #pragma unroll
                     for (int x = 0; x < 32; x++) mask |= (v[x] <= thr ? 1u : 0u) << x;
@@ -411,7 +421,7 @@ __device__ __forceinline__ int scale_exp(unsigned maxbits)
     if (!(mx > 0.f)) return 0;
     int ex;
     frexpf(mx, &ex);  // mx = f * 2^ex, f in [0.5, 1)
-    return 14 - ex;
+    return min(max(14 - ex, -60), 60);  // clamped: bounds stay finite in accumulator units
 }
 
 // fp16 operand rows: fl16(fl(x - c) * 2^S)
@@ -486,7 +496,7 @@ __global__ void exact_scal_kernel(const unsigned *__restrict__ maxq, const unsig
     const double aq = ldexp(1.0, -25 - Sa), ar = ldexp(1.0, -25 - Sb);
     s.eabs = (float)(8.0 * dim * (aq * mr + ar * mq + aq * ar) + 1e-30);
     s.E = E;
-    s.pad = 0.f;
+    s.hs = ldexpf(1.f, Sa + Sb - 1);
     *out = s;
 }
 

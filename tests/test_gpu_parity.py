@@ -412,3 +412,29 @@ def test_exact_tc_field_cfg3_sample(R):
     assert np.array_equal(ai, bi) and np.array_equal(_bits(ad), _bits(bd))
     _, _, checked, fb = _exact_stats(model, units)
     assert checked < 8 * len(units) and fb < len(units) // 100
+
+
+def test_model_switch_smaller_n(R, oracle_mod):
+    """A context reused for a model with fewer references: stale pool entries
+    from the larger model must never be used as indices (regression)."""
+    from dataclasses import replace
+
+    from paper_1508_07953_b200 import workloads as W
+
+    big = replace(W.CONFIGS[1], height=48, width=72, frames=2)
+    mb = R.ReferenceModel.from_refs(W.reference_set(W.CONFIGS[1]), big.patch)
+    for _ in R.stream_fields(mb, W.clip(big)):
+        pass
+    cfg = replace(W.CONFIGS[3], height=40, width=64, frames=3, n_refs=2048)
+    frames = W.clip(cfg)
+    refs = W.reference_set(cfg)
+    model = R.ReferenceModel.from_refs(refs, cfg.patch, channels=3)
+    sd, si = model.table_rows(0, model.n)
+    om = oracle_mod.OracleModel(refs, sd, si)
+    gw, gh = cfg.grid
+    prev = oracle_mod.init_field_indices(gw, gh, model.n, 0)
+    for t, (_, fld, st) in enumerate(R.stream_fields(model, frames)):
+        idx, dist, ost, _ = oracle_mod.process_frame(om, frames[t], prev, cfg.patch, t + 1)
+        assert np.array_equal(fld.indices, idx), t
+        assert np.array_equal(_bits(fld.distances), _bits(dist)), t
+        prev = idx

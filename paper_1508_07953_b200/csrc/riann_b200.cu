@@ -348,7 +348,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     // P0
     {
         const int wpb = 8;
-        const size_t smem = (size_t)wpb * 32 * (rb::p0_chunk_words(n) + 1) * 4;
+        const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
         auto k = rb::bulk_p0_kernel<D>;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int bps = 0;

@@ -202,9 +202,10 @@ __device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int cnt, uint3
 // P0: first ring, candidate slot, first anchor.  One warp per query.
 // The first-ring window (unordered: distance order) becomes the ascending
 // candidate list (np.sort, search.py:116) through a per-warp n-bit bitmap in
-// shared memory; each lane owns a contiguous chunk of words, padded by one
-// word so the lanes' chunks fall in different banks.
-__host__ __device__ constexpr int p0_chunk_words(int64_t n) { return (int)(((n + 31) / 32 + 31) / 32); }
+// shared memory, enumerated word-interleaved: at step t lane L takes word
+// 32t + L, a warp prefix sum places its bits, so each step's stores fall in
+// one short run of the slot.
+__host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 1023) / 1024) * 32); }
 
 template <int D>
 __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
@@ -214,12 +215,11 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int64_t n = P.n;
-    const int CW = p0_chunk_words(n);  // words per lane chunk
-    const int stride = CW + 1;         // padded
-    uint32_t *bm = smem_w + (size_t)wib * 32 * stride;
+    const int NW = p0_words(n);  // multiple of 32
+    uint32_t *bm = smem_w + (size_t)wib * NW;
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const int64_t gwarp = (int64_t)blockIdx.x * wpb + wib;
-    for (int i = lane; i < 32 * stride; i += 32) bm[i] = 0u;
+    for (int i = lane; i < NW; i += 32) bm[i] = 0u;
     __syncwarp();
     for (int64_t g = gwarp; g < P.Q; g += nwarps) {
         const float *q = P.units + g * D;
@@ -250,10 +250,7 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
         // window of the u16 index row -> bitmap (16-byte vector loads on the aligned span)
         {
             const uint16_t *row = P.sidx + (int64_t)p * n;
-            auto mark = [&](uint32_t j) {
-                const uint32_t w = j >> 5;
-                atomicOr(&bm[(w / CW) * stride + (w % CW)], 1u << (j & 31));
-            };
+            auto mark = [&](uint32_t j) { atomicOr(&bm[j >> 5], 1u << (j & 31)); };
             const int64_t a0 = (lo + 7) & ~(int64_t)7, a1 = hi & ~(int64_t)7;
             if (a0 < a1) {
                 for (int64_t k = lo + lane; k < a0; k += 32) mark(__ldg(row + k));
@@ -269,39 +266,34 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             }
         }
         __syncwarp();
-        // enumerate ascending into the slot; clear the bitmap
+        // enumerate ascending into the slot, clearing the bitmap; rank and presence of p
         uint16_t *slot = P.pool + off;
-        const uint32_t *mine = bm + lane * stride;
-        int cnt = 0;
-        for (int w = 0; w < CW; w++) cnt += __popc(mine[w]);
-        const int inc = warp_incl_scan(cnt, lane);
-        int o = inc - cnt;
-        // rank of p among S (its position if present) and presence
-        const uint32_t wp = (uint32_t)p >> 5;
-        const int lp = (int)(wp / CW);
-        int below = 0;
-        bool p_in = false;
-        if (lane == lp) {
-            below = o;
-            for (int w = 0; w < (int)(wp % CW); w++) below += __popc(mine[w]);
-            const uint32_t word = mine[wp % CW];
-            below += __popc(word & ((1u << (p & 31)) - 1u));
-            p_in = (word >> (p & 31)) & 1u;
-        }
-        below = __shfl_sync(FULL, below, lp);
-        p_in = __shfl_sync(FULL, (int)p_in, lp);
-        for (int w = 0; w < CW; w++) {
-            uint32_t word = bm[lane * stride + w];
-            if (word) {
-                bm[lane * stride + w] = 0u;
-                const uint32_t base = (uint32_t)(lane * CW + w) * 32u;
-                while (word) {
-                    const int b = __ffs(word) - 1;
-                    word &= word - 1;
-                    slot[o++] = (uint16_t)(base + b);
-                }
+        const int wp = p >> 5;
+        int run = 0, below = 0, p_in = 0;
+        for (int t = 0; t < NW; t += 32) {
+            const int w = t + lane;
+            uint32_t word = bm[w];
+            const unsigned any = __ballot_sync(FULL, word != 0u);
+            if (!any) continue;
+            if (word) bm[w] = 0u;
+            const int c = __popc(word);
+            const int inc = warp_incl_scan(c, lane);
+            int o = run + inc - c;
+            if (w == wp) {
+                below = o + __popc(word & ((1u << (p & 31)) - 1u));
+                p_in = (word >> (p & 31)) & 1u;
             }
+            const uint32_t base = (uint32_t)w * 32u;
+            while (word) {
+                const int b = __ffs(word) - 1;
+                word &= word - 1;
+                slot[o++] = (uint16_t)(base + b);
+            }
+            run += __shfl_sync(FULL, inc, 31);
         }
+        const int lp = (wp & 31);
+        below = __shfl_sync(FULL, below, lp);
+        p_in = __shfl_sync(FULL, p_in, lp);
         __threadfence_block();
         __syncwarp();
         if (lane == 0) {

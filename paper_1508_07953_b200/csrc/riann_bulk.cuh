@@ -627,6 +627,13 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
         auto lb_of = [&](float s, float sl) {
             return __fdiv_rd(__fsub_rd(__fsqrt_rd(__fmul_rd(s, 0.99997f)), sl), SP.one_plus_eta);
         };
+        // chunk test without sqrt/div: (sqrt(0.99997 s) - slack) / (1 + eta) <= ub  <=>
+        // s <= (ub (1 + eta) + slack)^2 / 0.99997; thr is that bound rounded up (a superset)
+        auto thr_of = [&](float ubv) {
+            const float r = __fadd_ru(__fmul_ru(ubv, SP.one_plus_eta), SP.slack);
+            return __fdiv_ru(__fmul_ru(r, r), 0.99997f);
+        };
+        float thr = thr_of(ub);
         for (int blk = 0; blk < cS; blk += FB) {
             const int bn = min(FB, cS - blk);
             // chunk 0 over the block, one candidate per lane
@@ -664,7 +671,7 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
                     s = __fmaf_rn(a0, a0, s);
                     s = __fmaf_rn(a1, a1, s);
                 }
-                const bool keep = valid && lb_of(s, SP.slack) <= ub;
+                const bool keep = valid && s <= thr;
                 const unsigned ball = __ballot_sync(FULL, keep);
                 if (keep) {
                     const int o = nA + __popc(ball & lanemask_lt());
@@ -711,7 +718,7 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
                         s = __fmaf_rn(a1, a1, s);
                     }
                     if (!last) {
-                        const bool keep = valid && lb_of(s, SP.slack) <= ub;
+                        const bool keep = valid && s <= thr;
                         const unsigned ball = __ballot_sync(FULL, keep);
                         if (keep) {
                             const int o = nB + __popc(ball & lanemask_lt());
@@ -729,7 +736,10 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
                         float mv = u;
 #pragma unroll
                         for (int o = 16; o >= 1; o >>= 1) mv = fminf(mv, __shfl_xor_sync(FULL, mv, o));
-                        ub = fminf(ub, mv);
+                        if (mv < ub) {
+                            ub = mv;
+                            thr = thr_of(ub);
+                        }
                         const float lb = lb_of(s, sl);
                         const bool surv = valid && lb <= ub;
                         const unsigned ball = __ballot_sync(FULL, surv);

@@ -404,7 +404,7 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigne
 // is read from HBM about once per phase); membership tests are 8-deep
 // independent lookups pos[a][j] per lane.
 template <int D>
-__global__ void __launch_bounds__(256, 3) bulk_ring_kernel(BulkParams P)
+__global__ void __launch_bounds__(256, 4) bulk_ring_kernel(BulkParams P)
 {
     const int lane = threadIdx.x & 31;
     const int64_t n = P.n;

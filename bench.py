@@ -311,11 +311,16 @@ def run_ours(a):
     gathered = None
     if world > 1:
         gathered = torch.empty((world, (gh // world + 1) * gw * 3), dtype=torch.int32, device="cuda")
+    # pinned output fields, two pairs used alternately (a frame's field stays valid
+    # until the frame after next), passed through the public API's out= arguments
+    outs = [(torch.empty((y1 - y0, gw), dtype=torch.int32, pin_memory=True).numpy(),
+             torch.empty((y1 - y0, gw), dtype=torch.float64, pin_memory=True).numpy()) for _ in range(2)]
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(K):
-        idx, dst, st = stream.step(host[Wm + k].numpy())
+        oi, od = outs[k & 1]
+        idx, dst, st = stream.step(host[Wm + k].numpy(), out_idx=oi, out_dist=od)
         fields.append((idx, dst, st))
         if world > 1:
             buf = torch.zeros((gh // world + 1) * gw * 3, dtype=torch.int32, device="cuda")

@@ -205,7 +205,7 @@ __device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int cnt, uint3
 // shared memory, enumerated word-interleaved: at step t lane L takes word
 // 32t + L, a warp prefix sum places its bits, so each step's stores fall in
 // one short run of the slot.
-__host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 1023) / 1024) * 32); }
+__host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 4095) / 4096) * 128); }
 
 template <int D>
 __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int64_t n = P.n;
-    const int NW = p0_words(n);  // multiple of 32
+    const int NW = p0_words(n);  // multiple of 128
     uint32_t *bm = smem_w + (size_t)wib * NW;
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const int64_t gwarp = (int64_t)blockIdx.x * wpb + wib;
@@ -266,32 +266,44 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             }
         }
         __syncwarp();
-        // enumerate ascending into the slot, clearing the bitmap; rank and presence of p
+        // enumerate ascending into the slot, clearing the bitmap; rank and presence of p.
+        // Step t: lane L takes words 128t + 4L .. +3 (one LDS.128); one warp scan per step.
         uint16_t *slot = P.pool + off;
         const int wp = p >> 5;
         int run = 0, below = 0, p_in = 0;
-        for (int t = 0; t < NW; t += 32) {
-            const int w = t + lane;
-            uint32_t word = bm[w];
-            const unsigned any = __ballot_sync(FULL, word != 0u);
-            if (!any) continue;
-            if (word) bm[w] = 0u;
-            const int c = __popc(word);
+        for (int t = 0; t < NW; t += 128) {
+            const int w0 = t + 4 * lane;
+            uint4 q4 = *reinterpret_cast<const uint4 *>(bm + w0);
+            const uint32_t any4 = q4.x | q4.y | q4.z | q4.w;
+            if (!__any_sync(FULL, any4 != 0u)) continue;
+            if (any4) *reinterpret_cast<uint4 *>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+            const int c = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
             const int inc = warp_incl_scan(c, lane);
             int o = run + inc - c;
-            if (w == wp) {
-                below = o + __popc(word & ((1u << (p & 31)) - 1u));
-                p_in = (word >> (p & 31)) & 1u;
+            if ((wp >> 2) == (w0 >> 2)) {  // this lane holds p's word
+                const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
+                int bb = o;
+                for (int k = 0; k < (wp & 3); k++) bb += __popc(wd[k]);
+                below = bb + __popc(wd[wp & 3] & ((1u << (p & 31)) - 1u));
+                p_in = (wd[wp & 3] >> (p & 31)) & 1u;
             }
-            const uint32_t base = (uint32_t)w * 32u;
-            while (word) {
-                const int b = __ffs(word) - 1;
-                word &= word - 1;
-                slot[o++] = (uint16_t)(base + b);
+            if (any4) {
+                uint16_t *dst = slot + o;
+                const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    uint32_t word = wd[k];
+                    const uint32_t base = (uint32_t)(w0 + k) * 32u;
+                    while (word) {
+                        const int b = __ffs(word) - 1;
+                        word &= word - 1;
+                        *dst++ = (uint16_t)(base + b);
+                    }
+                }
             }
             run += __shfl_sync(FULL, inc, 31);
         }
-        const int lp = (wp & 31);
+        const int lp = (wp >> 2) & 31;
         below = __shfl_sync(FULL, below, lp);
         p_in = __shfl_sync(FULL, p_in, lp);
         __threadfence_block();

@@ -179,6 +179,21 @@ int riann_exact_nn_device(riann_ctx *ctx, const float *queries, int64_t m,
 int riann_exact_field(riann_ctx *ctx, const float *frame, int H, int W, int C,
                       int32_t *out_idx, double *out_dist);
 
+/* ---- output side of the query ----------------------------- */
+/* One ANNF frame payload (engine.py:257-267) from the device-resident field:
+ * count little-endian u32 indices, then count f32 distances (f64 rounded to
+ * nearest), 8 * count bytes.  count must equal the field's position count. */
+int riann_field_pack(riann_ctx *ctx, void *payload, int64_t count);
+/* apply_effect / reconstruct_frame (transforms.py:192-253) on a single-plane
+ * frame (H, W): kind 0 reconstruction (payloads NULL = the model's refs,
+ * rescaled by each query patch's norm), 1 full-patch, 2 chroma-pair (payload
+ * width 2*pw*ph).  idx: (gh, gw) host matches, or NULL for the device field.
+ * out_planes (planes, H, W) f32 may be NULL; out_rgb (H, W, 3) u8 for kind 2.
+ * Bit-identical to numpy (same f32 add order, division and rounding). */
+int riann_apply_effect(riann_ctx *ctx, const float *frame, int H, int W,
+                       const int32_t *idx, const float *payloads, int64_t n_payloads,
+                       int payload_dim, int kind, float *out_planes, uint8_t *out_rgb);
+
 /* ---- host helpers ------------------------------------------------------ */
 /* init_field indices (engine.py:72-82): numpy default_rng(seed).integers(0,
  * n, (gh, gw), int32), bit-identical; seed given as SeedSequence words. */

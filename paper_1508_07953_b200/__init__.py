@@ -8,6 +8,7 @@ fallback: without the built library or a B200 the compute calls raise.
 """
 
 from ._native import current_device, set_device
+from .annf import ANNF_MAGIC, ANNF_VERSION, AnnfStream, AnnfWriter, read_annf, stream_to_annf
 from .engine import AnnField, FrameStats, frame_units, grid_shape, init_field, process_frame, stream_fields
 from .errors import DimensionError, FormatError, ModelCapacityError, RiannError
 from .evaluation import exact_nn, exact_nn_batch, field_exact_oracle
@@ -26,11 +27,23 @@ from .patches import (
     register_metric,
 )
 from .search import QueryResult, SearchParams, query_rng_key, riann_query, riann_query_batch, ring_candidates
+from .transforms import EffectTable, apply_effect, reconstruct_frame, reconstruction_error, reconstruction_table
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "ANNF_MAGIC",
+    "ANNF_VERSION",
     "AnnField",
+    "AnnfStream",
+    "AnnfWriter",
+    "EffectTable",
+    "apply_effect",
+    "read_annf",
+    "reconstruct_frame",
+    "reconstruction_error",
+    "reconstruction_table",
+    "stream_to_annf",
     "DEFAULT_REF_CAP",
     "DimensionError",
     "EUCLIDEAN",

@@ -24,6 +24,7 @@
 #include "riann_b200.h"
 #include "riann_bulk.cuh"
 #include "riann_exact_tc.cuh"
+#include "riann_effects.cuh"
 
 namespace {
 
@@ -190,6 +191,7 @@ struct riann_ctx {
     bool bulk_disabled = false;
     // K4 tensor-core comparator: split reference operand, norms, per-call scratch
     bool exact_simt = false, x_ready = false;
+    DevBuf fx_frame, fx_idx, fx_pay, fx_norm, fx_out, fx_rgb, pack;
     DevBuf x_B, x_nr, x_center, x_scal, x_A, x_nq, x_cand, x_lb, x_ncand, x_ub, x_fb, x_q, x_idx, x_dist;
     uint64_t x_checked = 0, x_fallback = 0;
     // bulk-path frame buffers
@@ -826,7 +828,8 @@ int riann_ctx_destroy(riann_ctx *c)
                       &c->tree.leaf_start, &c->tree.leaf_len, &c->tree.leaf_node, &c->tree.level_off,
                       &c->tree.inner, &c->tree.left, &c->tree.right, &c->tree.node_val, &c->x_B, &c->x_nr, &c->x_center, &c->x_scal,
                       &c->x_A, &c->x_nq, &c->x_cand, &c->x_lb, &c->x_ncand, &c->x_ub, &c->x_fb, &c->x_q,
-                      &c->x_idx, &c->x_dist};
+                      &c->x_idx, &c->x_dist, &c->fx_frame, &c->fx_idx, &c->fx_pay, &c->fx_norm, &c->fx_out,
+                      &c->fx_rgb, &c->pack};
     for (DevBuf *b : bufs) b->release();
     for (auto &a : c->ev_pending)
         for (auto e : a) cudaEventDestroy(e);
@@ -1726,6 +1729,98 @@ int riann_exact_field(riann_ctx *c, const float *frame, int H, int W, int C, int
     CK(cudaMemcpyAsync(out_idx, c->x_idx.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(out_dist, c->x_dist.p, (size_t)Q * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int riann_field_pack(riann_ctx *c, void *payload, int64_t count)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (c->field_count != count) return fail(RIANN_E_STATE, "no device field of %lld positions", (long long)count);
+    RET(c->use());
+    if (count <= 0) return 0;
+    RET(c->pack.ensure((size_t)count * 8));
+    rb::pack_field_kernel<<<(unsigned)((count + 255) / 256), 256, 0, c->stream>>>(
+        c->fld_idx[c->cur_fld].as<int32_t>(), c->fld_dist.as<double>(), count, c->pack.as<uint32_t>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(payload, c->pack.p, (size_t)count * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int riann_apply_effect(riann_ctx *c, const float *frame, int H, int W, const int32_t *idx, const float *payloads,
+                       int64_t n_payloads, int payload_dim, int kind, float *out_planes, uint8_t *out_rgb)
+{
+    RET(check_model(c, false));
+    if (kind < 0 || kind > 2) return fail(RIANN_E_VALUE, "unknown payload kind %d", kind);
+    if (c->C != 1 && !(c->pw * c->ph == c->dim))
+        return fail(RIANN_E_DIMENSION, "effects need a single-plane model (transforms.py:217-218)");
+    const int pw = c->pw, ph = c->ph, pp = pw * ph;
+    if (H < ph || W < pw) return fail(RIANN_E_DIMENSION, "frame %dx%d smaller than patch %dx%d", W, H, pw, ph);
+    const int planes = kind == rb::FX_CHROMA ? 2 : 1;
+    if (kind == rb::FX_RECONSTRUCTION && !payloads) {
+        n_payloads = c->n;
+        payload_dim = c->dim;
+    }
+    if (n_payloads != c->n)
+        return fail(RIANN_E_DIMENSION, "table holds %lld payloads for a model of %lld references",
+                    (long long)n_payloads, (long long)c->n);
+    if (payload_dim != planes * pp)
+        return fail(RIANN_E_DIMENSION, "payloads must be (n, %d), got width %d", planes * pp, payload_dim);
+    const int gw = W - pw + 1, gh = H - ph + 1;
+    const int64_t Q = (int64_t)gw * gh, P = (int64_t)H * W;
+    RET(c->use());
+    RET(c->fx_frame.ensure((size_t)P * 4));
+    CK(cudaMemcpyAsync(c->fx_frame.p, frame, (size_t)P * 4, cudaMemcpyHostToDevice, c->stream));
+    const int32_t *didx;
+    if (idx) {
+        RET(c->fx_idx.ensure((size_t)Q * 4));
+        CK(cudaMemcpyAsync(c->fx_idx.p, idx, (size_t)Q * 4, cudaMemcpyHostToDevice, c->stream));
+        didx = c->fx_idx.as<int32_t>();
+    } else {
+        if (c->field_count != Q)
+            return fail(RIANN_E_STATE, "no device field of %lld positions", (long long)Q);
+        didx = c->fld_idx[c->cur_fld].as<int32_t>();
+    }
+    const float *dpay = c->refs.as<float>();
+    if (payloads) {
+        RET(c->fx_pay.ensure((size_t)n_payloads * payload_dim * 4));
+        CK(cudaMemcpyAsync(c->fx_pay.p, payloads, (size_t)n_payloads * payload_dim * 4, cudaMemcpyHostToDevice,
+                           c->stream));
+        dpay = c->fx_pay.as<float>();
+    }
+    rb::BlendParams B{};
+    B.frame = c->fx_frame.as<float>();
+    B.H = H;
+    B.W = W;
+    B.pw = pw;
+    B.ph = ph;
+    B.gw = gw;
+    B.gh = gh;
+    B.idx = didx;
+    B.payloads = dpay;
+    B.planes = planes;
+    B.kind = kind;
+    if (kind == rb::FX_RECONSTRUCTION) {
+        RET(c->fx_norm.ensure((size_t)Q * 4));
+        rb::effect_norms_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, c->stream>>>(B.frame, H, W, pw, ph, gw, Q,
+                                                                                    c->fx_norm.as<float>());
+        CK(cudaGetLastError());
+        B.norm32 = c->fx_norm.as<float>();
+    }
+    if (out_planes) {
+        RET(c->fx_out.ensure((size_t)planes * P * 4));
+        B.out = c->fx_out.as<float>();
+    }
+    if (kind == rb::FX_CHROMA && out_rgb) {
+        RET(c->fx_rgb.ensure((size_t)P * 3));
+        B.rgb = c->fx_rgb.as<uint8_t>();
+    }
+    rb::blend_kernel<<<(unsigned)((P + 255) / 256), 256, 0, c->stream>>>(B);
+    CK(cudaGetLastError());
+    if (out_planes) CK(cudaMemcpyAsync(out_planes, B.out, (size_t)planes * P * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (B.rgb) CK(cudaMemcpyAsync(out_rgb, B.rgb, (size_t)P * 3, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->launches += 2;
     return 0;
 }
 

@@ -1,0 +1,118 @@
+// riann_effects.cuh -- the callers on the output side of the query:
+//   * ANNF frame payload (engine.py:257-267): idx as u32, dist as f32, packed on
+//     the device straight from the resident field (8 bytes per position leave
+//     the GPU instead of 12);
+//   * apply_effect / reconstruct_frame (transforms.py:175-253): gather each
+//     position's payload row by its match, rescale by the query norm
+//     (reconstruction kind), uniform average of the overlapping windows, and
+//     for the chroma kind the integer YCoCg -> RGB finish.
+// Every output is bit-identical to numpy: float32 adds in the reference's
+// (dy, dx) loop order starting from 0, one correctly rounded f32 division,
+// the f32/f64 rounding expressions of round_half_away.
+#pragma once
+
+#include "riann_kernels.cuh"
+
+namespace rb {
+
+enum { FX_RECONSTRUCTION = 0, FX_FULL = 1, FX_CHROMA = 2 };
+
+// payload of one ANNF frame: Q little-endian u32 indices, then Q f32 distances
+__global__ void pack_field_kernel(const int32_t *__restrict__ idx, const double *__restrict__ dist, int64_t Q,
+                                  uint32_t *__restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    out[i] = (uint32_t)idx[i];                                      // astype("<u4"): same bits for 0 <= idx < 2^31
+    out[Q + i] = __float_as_uint(__double2float_rn(dist[i]));       // astype("<f4"): round to nearest even
+}
+
+// f32(norm) of every query patch as normalize_rows computes it (patches.py:100-115):
+// sqrt of numpy's pairwise f64 sum of squares, 0 below 1e-12
+__global__ void effect_norms_kernel(const float *__restrict__ frame, int H, int W, int pw, int ph, int gw, int64_t Q,
+                                    float *__restrict__ norm32)
+{
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Q) return;
+    const int x = (int)(g % gw), y = (int)(g / gw);
+    FrameGet<0, 0> get{frame + (int64_t)y * W + x, W, 1, pw, ph};
+    const double nr = __dsqrt_rn(pw_sum(get, 0, (int64_t)pw * ph));
+    norm32[g] = nr >= 1e-12 ? __double2float_rn(nr) : 0.0f;
+}
+
+// round_half_away on a float32 value (numpy evaluates it in float32 for f32 input)
+__device__ __forceinline__ long long rha_f32(float x)
+{
+    const float a = floorf(__fadd_rn(fabsf(x), 0.5f));
+    const float s = x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f);
+    return (long long)__fmul_rn(s, a);
+}
+
+// round_half_away on a float64 value
+__device__ __forceinline__ long long rha_f64(double x)
+{
+    const double a = floor(__dadd_rn(fabs(x), 0.5));
+    const double s = x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0);
+    return (long long)__dmul_rn(s, a);
+}
+
+struct BlendParams {
+    const float *frame;       // (H, W) single plane
+    int H, W, pw, ph, gw, gh;
+    const int32_t *idx;       // (gh, gw) matches
+    const float *payloads;    // (n, planes * pw * ph)
+    int planes;               // 1 (reconstruction / full-patch) or 2 (chroma)
+    int kind;
+    const float *norm32;      // (gh * gw) for the reconstruction kind
+    float *out;               // (planes, H, W) f32, or null
+    uint8_t *rgb;             // (H, W, 3) for the chroma kind, or null
+};
+
+// _blend_planes (transforms.py:175-189) + the kind-specific finish (:230-253):
+// thread per output pixel; contributions summed in the reference's (dy, dx) order
+__global__ void blend_kernel(BlendParams P)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= (int64_t)P.H * P.W) return;
+    const int y = (int)(p / P.W), x = (int)(p - (int64_t)y * P.W);
+    const int pp = P.pw * P.ph;
+    float acc[2] = {0.f, 0.f};
+    float cnt = 0.f;
+    for (int dy = 0; dy < P.ph; dy++) {
+        const int gy = y - dy;
+        if (gy < 0 || gy >= P.gh) continue;
+        for (int dx = 0; dx < P.pw; dx++) {
+            const int gx = x - dx;
+            if (gx < 0 || gx >= P.gw) continue;
+            const int64_t g = (int64_t)gy * P.gw + gx;
+            const float *row = P.payloads + (int64_t)P.idx[g] * P.planes * pp + dy * P.pw + dx;
+            const float sc = P.kind == FX_RECONSTRUCTION ? P.norm32[g] : 1.f;
+            for (int c = 0; c < P.planes; c++) {
+                float v = __ldg(row + c * pp);
+                if (P.kind == FX_RECONSTRUCTION) v = __fmul_rn(v, sc);
+                acc[c] = __fadd_rn(acc[c], v);
+            }
+            cnt = __fadd_rn(cnt, 1.f);
+        }
+    }
+    float pl[2];
+    for (int c = 0; c < P.planes; c++) pl[c] = __fdiv_rn(acc[c], cnt);
+    if (P.out)
+        for (int c = 0; c < P.planes; c++) P.out[(int64_t)c * P.H * P.W + p] = pl[c];
+    if (P.kind == FX_CHROMA && P.rgb) {
+        // ycocg = (rha(frame * 255) f64, rha(co) f32, rha(cg) f32); ycocg_to_rgb; clip to u8
+        const long long Y = rha_f64(__dmul_rn((double)P.frame[p], 255.0));
+        const long long co = rha_f32(pl[0]), cg = rha_f32(pl[1]);
+        const long long t = Y - (cg >> 1);
+        const long long gg = cg + t;
+        const long long b = t - (co >> 1);
+        const long long r = b + co;
+        const long long v3[3] = {r, gg, b};
+        for (int c = 0; c < 3; c++) {
+            const long long v = v3[c] < 0 ? 0 : (v3[c] > 255 ? 255 : v3[c]);
+            P.rgb[p * 3 + c] = (uint8_t)v;
+        }
+    }
+}
+
+}  // namespace rb

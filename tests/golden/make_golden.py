@@ -19,6 +19,12 @@ Fixtures:
                       all outputs incl. scanned sets, many param settings.
   golden_cfg0.npz     config 0 end to end: stream_fields (engine.py:205-227)
                       over all 8 frames, every position, FrameStats.
+  golden_annf.npz     ANNF containers written by the reference AnnfWriter
+                      (engine.py:228-279) from the config-0 golden fields, and
+                      an empty stream.
+  golden_effects.npz  apply_effect (transforms.py:192-246) for the three
+                      payload kinds on the config-0 field and on a small
+                      non-square-patch model.
   golden_cfg1.npz /   configs 1-2: riann_query at a seeded sample of positions
   golden_cfg2.npz     through all 30 frames, exactly as engine.py:137-143
                       calls it (positions are independent).
@@ -299,6 +305,63 @@ def gen_vga(cfg_id, model=None, refs=None, npos=256):
     return model, refs
 
 
+def gen_annf():
+    import tempfile
+
+    from riann.engine import AnnField, AnnfWriter
+
+    g = np.load(os.path.join(HERE, "golden_cfg0.npz"))
+    idx, dist = g["idx"], g["dist"]
+    gh, gw = idx.shape[1:]
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "cfg0.annf")
+        with AnnfWriter(path, gw, gh, (8, 8)) as w:
+            for t in range(idx.shape[0]):
+                w.append(AnnField(width=gw, height=gh, indices=idx[t], distances=dist[t], frame_t=t + 1))
+        out["cfg0_bytes"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+        path = os.path.join(d, "empty.annf")
+        AnnfWriter(path, 7, 5, (8, 8)).close()
+        out["empty_bytes"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+    save("golden_annf.npz", **out)
+
+
+def gen_effects():
+    from riann.engine import AnnField
+    from riann.transforms import (KIND_CHROMA, KIND_FULL, EffectTable, apply_effect,
+                                  reconstruct_frame)
+
+    out = {}
+    # config 0: the golden field of the last frame
+    g = np.load(os.path.join(HERE, "golden_cfg0.npz"))
+    frame = g["frames"][-1]
+    model = make_model(g["refs"], (8, 8))
+    gh, gw = g["idx"].shape[1:]
+    field = AnnField(width=gw, height=gh, indices=g["idx"][-1], distances=g["dist"][-1], frame_t=8)
+    rng = np.random.default_rng(77)
+    full = rng.uniform(0, 1, size=(model.n, 64)).astype(np.float32)
+    chroma = rng.uniform(-60, 60, size=(model.n, 128)).astype(np.float32)
+    out["c0_recon"] = reconstruct_frame(frame, field, model)
+    out["c0_full_pay"] = full
+    out["c0_full"] = apply_effect(frame, field, EffectTable(full, KIND_FULL, (8, 8)), model)
+    out["c0_chroma_pay"] = chroma
+    out["c0_chroma"] = apply_effect(frame, field, EffectTable(chroma, KIND_CHROMA, (8, 8)), model)
+    # small model, non-square patch (pw=4, ph=3), random field
+    refs, _ = normalize_rows(rng.standard_normal((30, 12)).astype(np.float32))
+    sm = make_model(refs, (4, 3))
+    fr = rng.uniform(0, 1, size=(9, 11)).astype(np.float32)
+    fr[0:3, 0:4] = 0.0  # a zero patch: norm 0
+    sidx = rng.integers(0, 30, size=(9 - 3 + 1, 11 - 4 + 1), dtype=np.int32)
+    sf = AnnField(width=8, height=7, indices=sidx, distances=np.zeros((7, 8)), frame_t=1)
+    sfull = rng.uniform(-2, 2, size=(30, 12)).astype(np.float32)
+    schroma = rng.uniform(-300, 300, size=(30, 24)).astype(np.float32)
+    out.update(s_refs=refs, s_frame=fr, s_idx=sidx, s_full_pay=sfull, s_chroma_pay=schroma,
+               s_recon=reconstruct_frame(fr, sf, sm),
+               s_full=apply_effect(fr, sf, EffectTable(sfull, KIND_FULL, (4, 3)), sm),
+               s_chroma=apply_effect(fr, sf, EffectTable(schroma, KIND_CHROMA, (4, 3)), sm))
+    save("golden_effects.npz", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-vga", action="store_true")
@@ -306,7 +369,7 @@ def main():
     a = ap.parse_args()
     only = set(a.only.split(",")) if a.only else None
     steps = [("rng", gen_rng), ("arith", gen_arith), ("tables", gen_tables),
-             ("queries", gen_queries), ("cfg0", gen_cfg0)]
+             ("queries", gen_queries), ("cfg0", gen_cfg0), ("annf", gen_annf), ("effects", gen_effects)]
     for name, fn in steps:
         if only is None or name in only:
             fn()

@@ -1801,11 +1801,15 @@ int riann_apply_effect(riann_ctx *c, const float *frame, int H, int W, const int
     B.planes = planes;
     B.kind = kind;
     if (kind == rb::FX_RECONSTRUCTION) {
-        RET(c->fx_norm.ensure((size_t)Q * 4));
-        rb::effect_norms_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, c->stream>>>(B.frame, H, W, pw, ph, gw, Q,
-                                                                                    c->fx_norm.as<float>());
-        CK(cudaGetLastError());
-        B.norm32 = c->fx_norm.as<float>();
+        RET(c->fx_norm.ensure((size_t)Q * 8));
+        if (pw == 8 && ph == 8 && c->dim == 64) {  // warp-cooperative K1, norms only
+            RET(launch_units(c, B.frame, H, W, 1, nullptr, c->fx_norm.as<double>(), nullptr, nullptr));
+        } else {
+            rb::effect_norms_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, c->stream>>>(
+                B.frame, H, W, pw, ph, gw, Q, c->fx_norm.as<double>());
+            CK(cudaGetLastError());
+        }
+        B.norms = c->fx_norm.as<double>();
     }
     if (out_planes) {
         RET(c->fx_out.ensure((size_t)planes * P * 4));
@@ -1815,7 +1819,14 @@ int riann_apply_effect(riann_ctx *c, const float *frame, int H, int W, const int
         RET(c->fx_rgb.ensure((size_t)P * 3));
         B.rgb = c->fx_rgb.as<uint8_t>();
     }
-    rb::blend_kernel<<<(unsigned)((P + 255) / 256), 256, 0, c->stream>>>(B);
+    if (pw <= 16) {
+        const size_t sm = (size_t)planes * rb::BY * (rb::BX + pw - 1) * pw * 4;
+        CK(cudaFuncSetAttribute(rb::blend_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        const dim3 grid((unsigned)((W + rb::BX - 1) / rb::BX), (unsigned)((H + rb::BY - 1) / rb::BY));
+        rb::blend_tiled_kernel<<<grid, rb::BX * rb::BY, sm, c->stream>>>(B);
+    } else {
+        rb::blend_kernel<<<(unsigned)((P + 255) / 256), 256, 0, c->stream>>>(B);
+    }
     CK(cudaGetLastError());
     if (out_planes) CK(cudaMemcpyAsync(out_planes, B.out, (size_t)planes * P * 4, cudaMemcpyDeviceToHost, c->stream));
     if (B.rgb) CK(cudaMemcpyAsync(out_rgb, B.rgb, (size_t)P * 3, cudaMemcpyDeviceToHost, c->stream));

@@ -27,17 +27,18 @@ __global__ void pack_field_kernel(const int32_t *__restrict__ idx, const double 
     out[Q + i] = __float_as_uint(__double2float_rn(dist[i]));       // astype("<f4"): round to nearest even
 }
 
-// f32(norm) of every query patch as normalize_rows computes it (patches.py:100-115):
-// sqrt of numpy's pairwise f64 sum of squares, 0 below 1e-12
+// norm of every query patch as normalize_rows computes it (patches.py:100-115):
+// sqrt of numpy's pairwise f64 sum of squares, 0 below 1e-12 (any patch size;
+// 8x8 patches use the warp-cooperative K1 kernel instead)
 __global__ void effect_norms_kernel(const float *__restrict__ frame, int H, int W, int pw, int ph, int gw, int64_t Q,
-                                    float *__restrict__ norm32)
+                                    double *__restrict__ norms)
 {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= Q) return;
     const int x = (int)(g % gw), y = (int)(g / gw);
     FrameGet<0, 0> get{frame + (int64_t)y * W + x, W, 1, pw, ph};
     const double nr = __dsqrt_rn(pw_sum(get, 0, (int64_t)pw * ph));
-    norm32[g] = nr >= 1e-12 ? __double2float_rn(nr) : 0.0f;
+    norms[g] = nr >= 1e-12 ? nr : 0.0;
 }
 
 // round_half_away on a float32 value (numpy evaluates it in float32 for f32 input)
@@ -63,7 +64,7 @@ struct BlendParams {
     const float *payloads;    // (n, planes * pw * ph)
     int planes;               // 1 (reconstruction / full-patch) or 2 (chroma)
     int kind;
-    const float *norm32;      // (gh * gw) for the reconstruction kind
+    const double *norms;      // (gh * gw) f64 query norms, reconstruction kind (rows scaled by f32(norm))
     float *out;               // (planes, H, W) f32, or null
     uint8_t *rgb;             // (H, W, 3) for the chroma kind, or null
 };
@@ -86,7 +87,7 @@ __global__ void blend_kernel(BlendParams P)
             if (gx < 0 || gx >= P.gw) continue;
             const int64_t g = (int64_t)gy * P.gw + gx;
             const float *row = P.payloads + (int64_t)P.idx[g] * P.planes * pp + dy * P.pw + dx;
-            const float sc = P.kind == FX_RECONSTRUCTION ? P.norm32[g] : 1.f;
+            const float sc = P.kind == FX_RECONSTRUCTION ? __double2float_rn(P.norms[g]) : 1.f;
             for (int c = 0; c < P.planes; c++) {
                 float v = __ldg(row + c * pp);
                 if (P.kind == FX_RECONSTRUCTION) v = __fmul_rn(v, sc);
@@ -101,6 +102,94 @@ __global__ void blend_kernel(BlendParams P)
         for (int c = 0; c < P.planes; c++) P.out[(int64_t)c * P.H * P.W + p] = pl[c];
     if (P.kind == FX_CHROMA && P.rgb) {
         // ycocg = (rha(frame * 255) f64, rha(co) f32, rha(cg) f32); ycocg_to_rgb; clip to u8
+        const long long Y = rha_f64(__dmul_rn((double)P.frame[p], 255.0));
+        const long long co = rha_f32(pl[0]), cg = rha_f32(pl[1]);
+        const long long t = Y - (cg >> 1);
+        const long long gg = cg + t;
+        const long long b = t - (co >> 1);
+        const long long r = b + co;
+        const long long v3[3] = {r, gg, b};
+        for (int c = 0; c < 3; c++) {
+            const long long v = v3[c] < 0 ? 0 : (v3[c] > 255 ? 255 : v3[c]);
+            P.rgb[p * 3 + c] = (uint8_t)v;
+        }
+    }
+}
+
+// Tiled form of blend_kernel for pw <= 16 (the same sums, same order): a CTA owns
+// an output tile of BY x BX pixels; for each dy it stages, for every position that
+// feeds the tile at that dy, the dy-th line of its payload row (pw values per plane,
+// norm-scaled for the reconstruction kind) in shared memory; each pixel then adds
+// the dx = 0..pw-1 contributions from shared memory.  dy outer, dx inner, as
+// transforms.py:183-187 accumulates.
+constexpr int BX = 64, BY = 8;
+
+__global__ void __launch_bounds__(BX * BY) blend_tiled_kernel(BlendParams P)
+{
+    extern __shared__ float sline[];  // [planes][BY][pw][BX + pw - 1] (consecutive threads: consecutive words)
+    const int pw = P.pw, ph = P.ph, pp = pw * ph;
+    const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
+    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    const int x = x0 + tx, y = y0 + ty;
+    const int SX = BX + pw - 1;  // positions per staged row
+    float acc[2] = {0.f, 0.f};
+    float cnt = 0.f;
+    for (int dy = 0; dy < ph; dy++) {
+        // stage positions gy = y0 + r - dy (r < BY), gx = x0 - pw + 1 + s (s < SX)
+        __syncthreads();
+        for (int e = threadIdx.x; e < BY * SX; e += BX * BY) {
+            const int r = e / SX, sx = e - r * SX;
+            const int gy = y0 + r - dy, gx = x0 - pw + 1 + sx;
+            const bool ok = gy >= 0 && gy < P.gh && gx >= 0 && gx < P.gw;
+            const int64_t g = ok ? (int64_t)gy * P.gw + gx : 0;
+            const float *row = P.payloads + (ok ? (int64_t)P.idx[g] * P.planes * pp : 0) + dy * pw;
+            const float sc = (ok && P.kind == FX_RECONSTRUCTION) ? __double2float_rn(P.norms[g]) : 1.f;
+            for (int c = 0; c < P.planes; c++) {
+                float *dst = sline + ((size_t)c * BY + r) * pw * SX + sx;
+                if ((pw & 3) == 0) {  // 16-byte vectors: row offsets are multiples of 4 floats
+                    for (int d4 = 0; d4 < pw; d4 += 4) {
+                        float4 v = ok ? __ldg(reinterpret_cast<const float4 *>(row + c * pp + d4))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (P.kind == FX_RECONSTRUCTION) {
+                            v.x = __fmul_rn(v.x, sc);
+                            v.y = __fmul_rn(v.y, sc);
+                            v.z = __fmul_rn(v.z, sc);
+                            v.w = __fmul_rn(v.w, sc);
+                        }
+                        dst[(size_t)(d4 + 0) * SX] = v.x;
+                        dst[(size_t)(d4 + 1) * SX] = v.y;
+                        dst[(size_t)(d4 + 2) * SX] = v.z;
+                        dst[(size_t)(d4 + 3) * SX] = v.w;
+                    }
+                } else {
+                    for (int dx = 0; dx < pw; dx++) {
+                        float v = ok ? __ldg(row + c * pp + dx) : 0.f;
+                        if (P.kind == FX_RECONSTRUCTION) v = __fmul_rn(v, sc);
+                        dst[(size_t)dx * SX] = v;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const int gy = y - dy;
+        if (y < P.H && x < P.W && gy >= 0 && gy < P.gh) {
+            for (int dx = 0; dx < pw; dx++) {
+                const int gx = x - dx;
+                if (gx < 0 || gx >= P.gw) continue;
+                const int sx = gx - (x0 - pw + 1);
+                for (int c = 0; c < P.planes; c++)
+                    acc[c] = __fadd_rn(acc[c], sline[(((size_t)c * BY + ty) * pw + dx) * SX + sx]);
+                cnt = __fadd_rn(cnt, 1.f);
+            }
+        }
+    }
+    if (y >= P.H || x >= P.W) return;
+    const int64_t p = (int64_t)y * P.W + x;
+    float pl[2];
+    for (int c = 0; c < P.planes; c++) pl[c] = __fdiv_rn(acc[c], cnt);
+    if (P.out)
+        for (int c = 0; c < P.planes; c++) P.out[(int64_t)c * P.H * P.W + p] = pl[c];
+    if (P.kind == FX_CHROMA && P.rgb) {
         const long long Y = rha_f64(__dmul_rn((double)P.frame[p], 255.0));
         const long long co = rha_f32(pl[0]), cg = rha_f32(pl[1]);
         const long long t = Y - (cg >> 1);

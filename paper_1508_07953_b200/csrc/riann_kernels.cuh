@@ -110,6 +110,8 @@ __global__ void __launch_bounds__(256) units_warp_kernel(UnitsParams P)
         if (G == 16) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 8));
         const double nr = __dsqrt_rn(acc);
         const bool ok = nr >= 1e-12;
+        if (valid && P.norms && gl == 0) P.norms[g] = ok ? nr : 0.0;
+        if (!P.unit) continue;  // norms only (apply_effect)
         float u[PER];
 #pragma unroll
         for (int i = 0; i < PER; i++) u[i] = ok ? __double2float_rn(__ddiv_rn((double)v[i], nr)) : 0.0f;
@@ -117,7 +119,6 @@ __global__ void __launch_bounds__(256) units_warp_kernel(UnitsParams P)
             float *ur = P.unit + g * D + base;
 #pragma unroll
             for (int i = 0; i < PER; i++) ur[8 * i] = u[i];
-            if (P.norms && gl == 0) P.norms[g] = ok ? nr : 0.0;
         }
         if (P.tc) {
             const float *pr = P.prev_unit + gg * D + base;

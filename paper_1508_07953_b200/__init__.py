@@ -27,6 +27,7 @@ from .patches import (
     register_metric,
 )
 from .search import QueryResult, SearchParams, query_rng_key, riann_query, riann_query_batch, ring_candidates
+from .modelio import MODEL_MAGIC, MODEL_VERSION, deserialize_model, load_model, model_memory_bytes, save_model, serialize_model
 from .transforms import EffectTable, apply_effect, reconstruct_frame, reconstruction_error, reconstruction_table
 
 __version__ = "0.1.0"
@@ -44,6 +45,13 @@ __all__ = [
     "reconstruction_error",
     "reconstruction_table",
     "stream_to_annf",
+    "MODEL_MAGIC",
+    "MODEL_VERSION",
+    "deserialize_model",
+    "load_model",
+    "model_memory_bytes",
+    "save_model",
+    "serialize_model",
     "DEFAULT_REF_CAP",
     "DimensionError",
     "EUCLIDEAN",

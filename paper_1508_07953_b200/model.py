@@ -4,8 +4,8 @@ Mirrors ReferenceModel (reference model.py:56-83) and compute_sorted_lists
 (:162-189).  Tables live in HBM as float32 distances (the reference's float64
 values are float32-quantised, :178-179, so this is lossless) and int32
 indices; the GPU builds them bit-identically to compute_sorted_lists (K3).
-The clustering builders (:86-160, :192-395) and the RIAN file format
-(:398-456) are out of scope for this hot-path build.
+The clustering builders (:86-160, :192-395) are out of scope (SURVEY.md §2);
+the RIAN file format (:398-456) is in ``modelio.py``.
 """
 
 from __future__ import annotations

@@ -25,6 +25,8 @@ Fixtures:
   golden_effects.npz  apply_effect (transforms.py:192-246) for the three
                       payload kinds on the config-0 field and on a small
                       non-square-patch model.
+  golden_rian.npz     RIAN containers from the reference serialize_model
+                      (model.py:398-411) for two small models (one 3-channel).
   golden_cfg1.npz /   configs 1-2: riann_query at a seeded sample of positions
   golden_cfg2.npz     through all 30 frames, exactly as engine.py:137-143
                       calls it (positions are independent).
@@ -362,6 +364,25 @@ def gen_effects():
     save("golden_effects.npz", **out)
 
 
+def gen_rian():
+    from riann.model import serialize_model
+
+    rng = np.random.default_rng(91)
+    out = {}
+    for tag, n, patch, ch in (("a", 40, (4, 4), 1), ("b", 30, (2, 2), 3)):
+        dim = patch[0] * patch[1] * ch
+        raw = rng.standard_normal((n, dim)).astype(np.float32)
+        raw[5] = raw[3]  # an exact duplicate: ties in the sorted rows
+        refs, _ = normalize_rows(raw)
+        sd, si = compute_sorted_lists(refs)
+        m = ReferenceModel(refs=refs, sorted_dist=sd, sorted_idx=si, patch_size=patch, channels=ch)
+        out[f"{tag}_refs"] = refs
+        out[f"{tag}_bytes"] = np.frombuffer(serialize_model(m), np.uint8)
+        out[f"{tag}_patch"] = np.array(patch)
+        out[f"{tag}_channels"] = np.array(ch)
+    save("golden_rian.npz", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-vga", action="store_true")
@@ -369,7 +390,8 @@ def main():
     a = ap.parse_args()
     only = set(a.only.split(",")) if a.only else None
     steps = [("rng", gen_rng), ("arith", gen_arith), ("tables", gen_tables),
-             ("queries", gen_queries), ("cfg0", gen_cfg0), ("annf", gen_annf), ("effects", gen_effects)]
+             ("queries", gen_queries), ("cfg0", gen_cfg0), ("annf", gen_annf), ("effects", gen_effects),
+             ("rian", gen_rian)]
     for name, fn in steps:
         if only is None or name in only:
             fn()

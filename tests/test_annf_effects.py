@@ -171,3 +171,54 @@ def test_apply_effect_golden(R):
     assert np.array_equal(out, g["s_chroma"])
     err = T.reconstruction_error(frame, T.reconstruct_frame(frame, field, model))
     assert 0.0 < err < 1.0
+
+
+# ---- RIAN model container (model.py:398-461) -----------------------------------
+def test_rian_host_round_trip(R, tmp_path):
+    g = load_golden("golden_rian.npz")
+    for tag in ("a", "b"):
+        blob = g[f"{tag}_bytes"].tobytes()
+        m = R.deserialize_model(blob)
+        assert np.array_equal(m.refs, g[f"{tag}_refs"]) and m.channels == int(g[f"{tag}_channels"])
+        assert m.sorted_dist.dtype == np.float64 and m.sorted_idx.dtype == np.int32
+        assert R.serialize_model(m) == blob
+        p = tmp_path / f"{tag}.rian"
+        R.save_model(p, m)
+        assert p.read_bytes() == blob
+        lm = R.load_model(p)
+        assert np.array_equal(lm.refs, m.refs) and np.array_equal(np.asarray(lm.sorted_idx), m.sorted_idx)
+        assert np.array_equal(np.asarray(lm.sorted_dist, np.float64), m.sorted_dist)
+        assert R.model_memory_bytes(m.n, m.dim) == len(blob) - 16
+
+
+def test_rian_errors(R, tmp_path):
+    blob = load_golden("golden_rian.npz")["a_bytes"].tobytes()
+    with pytest.raises(R.FormatError):
+        R.deserialize_model(blob[:10])
+    with pytest.raises(R.FormatError):
+        R.deserialize_model(b"JUNK" + blob[4:])
+    with pytest.raises(R.FormatError):
+        R.deserialize_model(blob[:4] + struct.pack("<H", 7) + blob[6:])
+    with pytest.raises(R.FormatError):
+        R.deserialize_model(blob[:-4])
+    p = tmp_path / "cut.rian"
+    p.write_bytes(blob[:-4])
+    with pytest.raises(R.FormatError):
+        R.load_model(p)
+
+
+@pytest.mark.gpu
+def test_rian_gpu_tables_byte_identical(R, tmp_path):
+    """Tables built on the GPU (K3) stream into a file byte-identical to the
+    reference's serialize_model; a mapped model uploads without a rebuild."""
+    g = load_golden("golden_rian.npz")
+    for tag in ("a", "b"):
+        m = R.ReferenceModel.from_refs(g[f"{tag}_refs"], tuple(int(v) for v in g[f"{tag}_patch"]),
+                                       channels=int(g[f"{tag}_channels"]))
+        p = tmp_path / f"{tag}.rian"
+        R.save_model(p, m)
+        assert p.read_bytes() == g[f"{tag}_bytes"].tobytes()
+        lm = R.load_model(p)
+        sd, si = lm.table_rows(0, lm.n)
+        ref = R.deserialize_model(g[f"{tag}_bytes"].tobytes())
+        assert np.array_equal(sd.astype(np.float64), ref.sorted_dist) and np.array_equal(si, ref.sorted_idx)

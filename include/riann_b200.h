@@ -194,6 +194,12 @@ int riann_apply_effect(riann_ctx *ctx, const float *frame, int H, int W,
                        const int32_t *idx, const float *payloads, int64_t n_payloads,
                        int payload_dim, int kind, float *out_planes, uint8_t *out_rgb);
 
+/* coherency_stats support (evaluation.py:86-138): for m index pairs,
+ * out_ab[k] = dist(refs[ia[k]], refs[ib[k]]) and, when u (m, dim) is given,
+ * out_au[k] = dist(refs[ia[k]], u[k]) -- numpy-order float64 distances. */
+int riann_pair_dist(riann_ctx *ctx, const int32_t *ia, const int32_t *ib,
+                    const float *u, int64_t m, double *out_ab, double *out_au);
+
 /* ---- host helpers ------------------------------------------------------ */
 /* init_field indices (engine.py:72-82): numpy default_rng(seed).integers(0,
  * n, (gh, gw), int32), bit-identical; seed given as SeedSequence words. */

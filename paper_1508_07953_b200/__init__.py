@@ -11,7 +11,7 @@ from ._native import current_device, set_device
 from .annf import ANNF_MAGIC, ANNF_VERSION, AnnfStream, AnnfWriter, read_annf, stream_to_annf
 from .engine import AnnField, FrameStats, frame_units, grid_shape, init_field, process_frame, stream_fields
 from .errors import DimensionError, FormatError, ModelCapacityError, RiannError
-from .evaluation import exact_nn, exact_nn_batch, field_exact_oracle
+from .evaluation import CoherencyStats, coherency_stats, exact_nn, exact_nn_batch, field_exact_oracle
 from .model import DEFAULT_REF_CAP, ReferenceModel, compute_sorted_lists
 from .patches import (
     EUCLIDEAN,
@@ -45,6 +45,8 @@ __all__ = [
     "reconstruction_error",
     "reconstruction_table",
     "stream_to_annf",
+    "CoherencyStats",
+    "coherency_stats",
     "MODEL_MAGIC",
     "MODEL_VERSION",
     "deserialize_model",

@@ -75,6 +75,7 @@ SIGNATURES = {
     "riann_exact_field": (i32, [P, P, i32, i32, i32, P, P]),
     "riann_field_pack": (i32, [P, P, i64]),
     "riann_apply_effect": (i32, [P, P, i32, i32, P, P, i64, i32, i32, P, P]),
+    "riann_pair_dist": (i32, [P, P, P, P, i64, P, P]),
     "riann_init_field": (i32, [i32, i32, i64, P, i32, P]),
     "riann_pairwise_sum": (dbl, [P, i64]),
 }

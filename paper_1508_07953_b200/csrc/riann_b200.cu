@@ -1835,6 +1835,39 @@ int riann_apply_effect(riann_ctx *c, const float *frame, int H, int W, const int
     return 0;
 }
 
+int riann_pair_dist(riann_ctx *c, const int32_t *ia, const int32_t *ib, const float *u, int64_t m, double *out_ab,
+                    double *out_au)
+{
+    RET(check_model(c, false));
+    if (m < 0) return fail(RIANN_E_VALUE, "negative pair count");
+    if (m == 0) return 0;
+    RET(c->use());
+    DevBuf di, dj, du, dab, dau;
+    RET(di.ensure((size_t)m * 4));
+    RET(dj.ensure((size_t)m * 4));
+    RET(dab.ensure((size_t)m * 8));
+    CK(cudaMemcpyAsync(di.p, ia, (size_t)m * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dj.p, ib, (size_t)m * 4, cudaMemcpyHostToDevice, c->stream));
+    if (u) {
+        RET(du.ensure((size_t)m * c->dim * 4));
+        RET(dau.ensure((size_t)m * 8));
+        CK(cudaMemcpyAsync(du.p, u, (size_t)m * c->dim * 4, cudaMemcpyHostToDevice, c->stream));
+    }
+    const unsigned blocks = (unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)c->sms * 16);
+    const float *dup = u ? du.as<float>() : nullptr;
+    switch (c->dim) {
+    case 16: rb::pair_dist_kernel<16><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), di.as<int32_t>(), dj.as<int32_t>(), dup, m, c->dim, dab.as<double>(), dau.as<double>()); break;
+    case 64: rb::pair_dist_kernel<64><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), di.as<int32_t>(), dj.as<int32_t>(), dup, m, c->dim, dab.as<double>(), dau.as<double>()); break;
+    case 192: rb::pair_dist_kernel<192><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), di.as<int32_t>(), dj.as<int32_t>(), dup, m, c->dim, dab.as<double>(), dau.as<double>()); break;
+    default: rb::pair_dist_kernel<0><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), di.as<int32_t>(), dj.as<int32_t>(), dup, m, c->dim, dab.as<double>(), dau.as<double>()); break;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_ab, dab.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (u && out_au) CK(cudaMemcpyAsync(out_au, dau.p, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
 int riann_init_field(int gw, int gh, int64_t n, const uint32_t *seed_words, int nwords, int32_t *out)
 {
     if (n < 1) return fail(RIANN_E_VALUE, "need at least one reference, got n=%lld", (long long)n);

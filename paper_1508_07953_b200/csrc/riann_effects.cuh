@@ -204,4 +204,39 @@ __global__ void __launch_bounds__(BX * BY) blend_tiled_kernel(BlendParams P)
     }
 }
 
+// coherency_stats (evaluation.py:86-138): for index pairs (i, j) and query rows u,
+// shift = dist(refs[i], refs[j]) and predictor = dist(refs[i], u), each the
+// numpy-order f64 distance of EuclideanMetric.__call__ (patches.py:138-159).
+// Warp-cooperative for numpy-mappable dims (groups of Lay<D>::G lanes).
+template <int D>
+__global__ void __launch_bounds__(256) pair_dist_kernel(const float *__restrict__ refs, const int32_t *__restrict__ ia,
+                                                        const int32_t *__restrict__ ib, const float *__restrict__ u,
+                                                        int64_t m, int dim, double *__restrict__ out_ab,
+                                                        double *__restrict__ out_au)
+{
+    constexpr int GX = D > 0 ? Lay<D>::G : 1;
+    constexpr int NG = WARP / GX;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k0 = w0 * NG; k0 < m; k0 += nw * NG) {
+        const int64_t k = k0 + lane / GX;
+        const bool ok = k < m;
+        const int64_t kk = ok ? k : 0;
+        const float *ri = refs + (int64_t)ia[kk] * dim;
+        double dab, dau = 0.0;
+        if constexpr (D > 0) {
+            dab = exact_dist<D>(refs, ib[kk], ri, D, lane % GX);
+            if (u) dau = exact_dist<D>(refs, ia[kk], u + kk * D, D, lane % GX);
+        } else {
+            dab = dist_thread(refs + (int64_t)ib[kk] * dim, ri, dim);
+            if (u) dau = dist_thread(u + kk * dim, ri, dim);
+        }
+        if (ok && (lane % GX) == 0) {
+            out_ab[k] = dab;
+            if (u) out_au[k] = dau;
+        }
+    }
+}
+
 }  // namespace rb

@@ -25,6 +25,8 @@ Fixtures:
   golden_effects.npz  apply_effect (transforms.py:192-246) for the three
                       payload kinds on the config-0 field and on a small
                       non-square-patch model.
+  golden_coherency.npz coherency_stats (evaluation.py:86-138) on the first 4
+                      config-0 frames (exact fields, shift/residual samples).
   golden_rian.npz     RIAN containers from the reference serialize_model
                       (model.py:398-411) for two small models (one 3-channel).
   golden_cfg1.npz /   configs 1-2: riann_query at a seeded sample of positions
@@ -383,6 +385,18 @@ def gen_rian():
     save("golden_rian.npz", **out)
 
 
+def gen_coherency():
+    from riann.evaluation import coherency_stats
+
+    cfg = W.CONFIGS[0]
+    frames = W.clip(cfg)[:4]
+    model = make_model(W.reference_set(cfg), cfg.patch)
+    st = coherency_stats(frames, model)
+    save("golden_coherency.npz", shift_samples=st.shift_samples, residual_samples=st.residual_samples,
+         shift_hist=st.shift_hist, shift_edges=st.shift_edges, residual_hist=st.residual_hist,
+         residual_edges=st.residual_edges, excluded=np.array(st.excluded))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-vga", action="store_true")
@@ -391,7 +405,7 @@ def main():
     only = set(a.only.split(",")) if a.only else None
     steps = [("rng", gen_rng), ("arith", gen_arith), ("tables", gen_tables),
              ("queries", gen_queries), ("cfg0", gen_cfg0), ("annf", gen_annf), ("effects", gen_effects),
-             ("rian", gen_rian)]
+             ("rian", gen_rian), ("coherency", gen_coherency)]
     for name, fn in steps:
         if only is None or name in only:
             fn()

@@ -222,3 +222,26 @@ def test_rian_gpu_tables_byte_identical(R, tmp_path):
         sd, si = lm.table_rows(0, lm.n)
         ref = R.deserialize_model(g[f"{tag}_bytes"].tobytes())
         assert np.array_equal(sd.astype(np.float64), ref.sorted_dist) and np.array_equal(si, ref.sorted_idx)
+
+
+# ---- exact-field statistics (evaluation.py:86-138) ------------------------------
+def test_coherency_validation(R):
+    with pytest.raises(ValueError):
+        R.coherency_stats([np.zeros((16, 16), np.float32)], None)
+    with pytest.raises(ValueError):
+        R.coherency_stats([np.zeros((16, 16), np.float32)] * 2, None, bin_width=0)
+
+
+@pytest.mark.gpu
+def test_coherency_stats_golden(R):
+    from paper_1508_07953_b200 import workloads as W
+
+    g = load_golden("golden_coherency.npz")
+    cfg = W.CONFIGS[0]
+    model = R.ReferenceModel.from_refs(W.reference_set(cfg), cfg.patch)
+    st = R.coherency_stats(W.clip(cfg)[:4], model)
+    assert st.excluded == int(g["excluded"]) and st.samples == g["shift_samples"].size
+    assert np.array_equal(st.shift_samples.view(np.uint64), g["shift_samples"].view(np.uint64))
+    assert np.array_equal(st.residual_samples.view(np.uint64), g["residual_samples"].view(np.uint64))
+    for k in ("shift_hist", "shift_edges", "residual_hist", "residual_edges"):
+        assert np.array_equal(getattr(st, k), g[k]), k

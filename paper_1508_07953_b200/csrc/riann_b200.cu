@@ -172,7 +172,8 @@ struct riann_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;  // heavy-query fallback, concurrent with the ring phases
-    cudaEvent_t ev_p0 = nullptr, ev_heavy = nullptr;
+    cudaStream_t stream3 = nullptr;  // final-scan projection, concurrent with P0 / ring phases
+    cudaEvent_t ev_p0 = nullptr, ev_heavy = nullptr, ev_units = nullptr, ev_proj = nullptr;
     int sms = 0;
     int smem_optin = 0;
     // model
@@ -347,6 +348,19 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.stats = Pq.stats;
     B.err = Pq.err;
 
+    // projection for the final scan (q' = T^T q, cuBLAS SGEMM, pedantic fp32) on a
+    // third stream: it needs only the unit rows, so it overlaps P0 and the rings
+    RET(c->units_pca.ensure((size_t)QN * D * 4));
+    CK(cudaEventRecord(c->ev_units, c->stream));
+    CK(cudaStreamWaitEvent(c->stream3, c->ev_units, 0));
+    {
+        CK(cublasSetStream(c->cublas, c->stream3) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
+        const float one = 1.f, zero = 0.f;
+        if (cublasSgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)QN, D, &one, c->pca_T.as<float>(), D, Pq.units,
+                        D, &zero, c->units_pca.as<float>(), D) != CUBLAS_STATUS_SUCCESS)
+            return fail(RIANN_E_CUDA, "cublasSgemm failed");
+        CK(cudaEventRecord(c->ev_proj, c->stream3));
+    }
     // P0
     {
         const int wpb = 8;
@@ -419,12 +433,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     }
     // final scan of the light queries (PCA-basis screening)
     {
-        RET(c->units_pca.ensure((size_t)QN * D * 4));
-        CK(cublasSetStream(c->cublas, c->stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
-        const float one = 1.f, zero = 0.f;
-        if (cublasSgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)QN, D, &one, c->pca_T.as<float>(), D, Pq.units,
-                        D, &zero, c->units_pca.as<float>(), D) != CUBLAS_STATUS_SUCCESS)
-            return fail(RIANN_E_CUDA, "cublasSgemm failed");
+        CK(cudaStreamWaitEvent(c->stream, c->ev_proj, 0));
         rb::ScreenParams SP;
         SP.refs_pca16 = c->refs_pca16.as<__half>();
         SP.e16p = c->e16p.as<float>();
@@ -801,6 +810,9 @@ int riann_ctx_create(int device, riann_ctx **out)
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p0, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_heavy, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_units, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_proj, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         delete c;
         return fail(RIANN_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
@@ -836,9 +848,13 @@ int riann_ctx_destroy(riann_ctx *c)
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->cublas) cublasDestroy(c->cublas);
     cudaStreamSynchronize(c->stream2);
+    cudaStreamSynchronize(c->stream3);
     cudaEventDestroy(c->ev_p0);
     cudaEventDestroy(c->ev_heavy);
+    cudaEventDestroy(c->ev_units);
+    cudaEventDestroy(c->ev_proj);
     cudaStreamDestroy(c->stream2);
+    cudaStreamDestroy(c->stream3);
     cudaStreamDestroy(c->stream);
     delete c;
     return 0;

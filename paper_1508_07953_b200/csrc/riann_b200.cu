@@ -182,13 +182,13 @@ struct riann_ctx {
     bool tables = false;
     bool idx16 = false;  // sorted index table stored as uint16 (n <= 65536)
     DevBuf refs, refs16, err16, sdist, sidx, dmat;
-    DevBuf pos, coarse;  // rank rows and coarse index (bulk path, n <= 65536)
+    DevBuf pos, coarse, coarse1;  // rank rows and two-level coarse index (bulk path, n <= 65536)
     // PCA screening basis (bulk final scan)
     DevBuf pca_T, refs_pca16, e16p, units_pca, e16max;
     bool pca = false;
     float pca_dq = 0.f, pca_eta = 0.f, pca_e16max = 0.f;
     cublasHandle_t cublas = nullptr;
-    int ncoarse = 0;
+    int ncoarse = 0, cs1 = 0;
     bool bulk_disabled = false;
     // K4 tensor-core comparator: split reference operand, norms, per-call scratch
     bool exact_simt = false, x_ready = false;
@@ -196,7 +196,7 @@ struct riann_ctx {
     DevBuf x_B, x_nr, x_center, x_scal, x_A, x_nq, x_cand, x_lb, x_ncand, x_ub, x_fb, x_q, x_idx, x_dist;
     uint64_t x_checked = 0, x_fallback = 0;
     // bulk-path frame buffers
-    DevBuf b_state, b_pool, b_p0spill, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_grouped,
+    DevBuf b_state, b_pool, b_bits, b_kept, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_gdesc,
         b_scan_tmp, overflow2;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
@@ -237,7 +237,7 @@ struct riann_ctx {
     }
     uint64_t bytes() const
     {
-        uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + pos.cap + coarse.cap + b_state.cap + pca_T.cap +
+        uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + pos.cap + coarse.cap + coarse1.cap + b_state.cap + pca_T.cap +
                      refs_pca16.cap + e16p.cap + units_pca.cap +
                      b_pool.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
                      fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap + x_B.cap + x_A.cap +
@@ -290,12 +290,13 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     // candidate pool: sum of first-ring sizes, capped (overflowing queries fall back to K2)
     const size_t pool_entries = std::min<size_t>((size_t)QN * 8192, (size_t)6 << 30);
     RET(c->b_pool.ensure(pool_entries * 2));
-    RET(c->b_p0spill.ensure((size_t)c->sms * 8 * 8 * 2 * rb::LIGHT_MAX * 2));
+    RET(c->b_bits.ensure(pool_entries / 4));  // two alive-bit buffers
+    RET(c->b_kept.ensure((size_t)QN * 4));
     RET(c->b_active[0].ensure((size_t)QN * 4));
     RET(c->b_active[1].ensure((size_t)QN * 4));
     RET(c->b_heavy.ensure((size_t)QN * 4));
     RET(c->b_heavy2.ensure((size_t)QN * 4));
-    RET(c->b_grouped.ensure((size_t)QN * 4));
+    RET(c->b_gdesc.ensure((size_t)QN * 16));
     RET(c->b_counters.ensure(256));
     RET(c->b_counts.ensure((size_t)(n + 1) * 4));
     RET(c->b_starts.ensure((size_t)(n + 1) * 4));
@@ -316,6 +317,8 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.sidx = c->sidx.as<uint16_t>();
     B.pos = c->pos.as<uint16_t>();
     B.coarse = c->coarse.as<float>();
+    B.coarse1 = c->coarse1.as<float>();
+    B.cs1 = c->cs1;
     B.n = n;
     B.ncoarse = c->ncoarse;
     B.units = Pq.units;
@@ -335,14 +338,15 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.pool = c->b_pool.as<uint16_t>();
     B.pool_top = reinterpret_cast<unsigned long long *>(ctr + 4);
     B.pool_cap = (int64_t)pool_entries;
-    B.p0_spill = c->b_p0spill.as<uint16_t>();
+    B.bits0 = c->b_bits.as<uint8_t>();
+    B.bits1 = B.bits0 + pool_entries / 8;
+    B.kept = c->b_kept.as<int32_t>();
     B.heavy = c->b_heavy.as<int32_t>();
     B.n_heavy = ctr + 2;
     B.counts = c->b_counts.as<int32_t>();
     B.starts = c->b_starts.as<int32_t>();
-    B.grouped = c->b_grouped.as<int32_t>();
+    B.gdesc = c->b_gdesc.as<int4>();
     B.item_next = ctr + 3;
-    B.seg_next = ctr + 16;
     B.out_idx = Pq.out_idx;
     B.out_dist = Pq.out_dist;
     B.stats = Pq.stats;
@@ -398,11 +402,17 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cudaEventRecord(c->ev_heavy, c->stream2));
     B.heavy = c->b_heavy2.as<int32_t>();
     B.n_heavy = ctr + 6;
-    // ring phases
-    auto rk = rb::bulk_ring_kernel<D>;
-    int ring_bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ring_bps, rk, 256, 0));
-    const unsigned ring_grid = (unsigned)(c->sms * std::max(ring_bps, 1));
+    // ring phases: group by anchor -> filter (anchor rows through shared memory) -> draw
+    auto fk = rb::bulk_filter_kernel;
+    const size_t fsmem = rb::filter_smem(n);
+    CK(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+    int f_bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f_bps, fk, rb::FW2 * 32, fsmem));
+    const unsigned f_grid = (unsigned)(c->sms * std::max(f_bps, 1));
+    auto dk = rb::bulk_draw_kernel<D>;
+    int d_bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d_bps, dk, 256, 0));
+    const unsigned d_grid = (unsigned)(c->sms * std::max(d_bps, 1));
     const unsigned small_grid = (unsigned)c->sms * 4;
     const int phases = Pq.max_rings - 1;
     for (int ph = 0; ph < phases; ph++) {
@@ -419,7 +429,6 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         }
         CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
         CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
-        CK(cudaMemsetAsync(ctr + 16, 0, 16 * 4, c->stream));
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
@@ -427,9 +436,11 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
-        rk<<<ring_grid, 256, 0, c->stream>>>(B);
+        fk<<<f_grid, rb::FW2 * 32, fsmem, c->stream>>>(B, ph & 1);
         CK(cudaGetLastError());
-        c->launches += 3;
+        dk<<<d_grid, 256, 0, c->stream>>>(B, ph & 1);
+        CK(cudaGetLastError());
+        c->launches += 4;
     }
     // final scan of the light queries (PCA-basis screening)
     {
@@ -469,7 +480,7 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
     P.passes = (bits + 7) / 8;
     if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && c->pca && !c->bulk_disabled &&
-        (c->dim == 64 || c->dim == 192) && c->n % 8 == 0) {
+        (c->dim == 64 || c->dim == 192) && c->n % 16 == 0) {
         int r = c->dim == 64 ? run_bulk_t<64>(c, P) : run_bulk_t<192>(c, P);
         if (r != 1) return r;
         // falls through: P.qlist = heavy queries
@@ -634,6 +645,11 @@ int build_bulk_tables(riann_ctx *c)
     const int64_t mc = n * c->ncoarse;
     rb::coarse_kernel<<<(unsigned)((mc + 255) / 256), 256, 0, c->stream>>>(c->sdist.as<float>(), n, c->ncoarse,
                                                                           c->coarse.as<float>());
+    CK(cudaGetLastError());
+    c->cs1 = (c->ncoarse + 31) / 32;
+    RET(c->coarse1.ensure((size_t)n * 32 * 4));
+    rb::coarse1_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, c->stream>>>(c->coarse.as<float>(), n, c->ncoarse,
+                                                                             c->cs1, c->coarse1.as<float>());
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     return 0;
@@ -830,9 +846,9 @@ int riann_ctx_destroy(riann_ctx *c)
     if (!c) return 0;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->b_state, &c->b_pool,
+    DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->coarse1, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_grouped, &c->b_scan_tmp, &c->b_p0spill, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
+                      &c->b_gdesc, &c->b_scan_tmp, &c->b_bits, &c->b_kept, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
                       &c->units_pca, &c->e16max, &c->snap_idx, &c->snap_units, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
@@ -899,6 +915,7 @@ int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, in
     c->dmat.release();
     c->pos.release();
     c->coarse.release();
+    c->coarse1.release();
     c->tables = false;
     c->x_ready = false;
     RET(c->refs.ensure((size_t)n * dim * 4));

@@ -1,22 +1,31 @@
 // riann_bulk.cuh -- anchor-grouped ("bulk") frame path for models with n <= 65,536.
 //
 // The per-query kernel (K2) pays one random DRAM fetch (~64 B) per ring
-// membership test: ~4,000 tests per query at config 3.  Here the frame runs in
+// membership test: ~5,000 tests per query at config 3.  Here the frame runs in
 // phases instead:
 //   P0   (warp per query): exact d_prev, first-ring window (coarse + fine
-//        search), window copy + radix sort into the query's candidate slot,
-//        first anchor draw (numpy RNG).
-//   ring phase k (<= max_rings-1 times): active queries are bucketed by their
-//        anchor (counting sort); one CTA loads an anchor's rank row
-//        pos[a][*] (u16, 128 KB) into shared memory once and filters the
-//        candidate lists of every query that drew that anchor (lo <= pos[a][j]
-//        < hi is exactly the searchsorted window test), then draws each
-//        query's next anchor.
+//        search), the window as an ascending fixed list (np.sort,
+//        search.py:116) split in two parts (j < n/2, j >= n/2, each padded to 8
+//        entries) with an alive bitmap, first anchor draw (numpy RNG), exact
+//        d_a and the anchor's window.
+//   ring phase k (<= max_rings-1 times):
+//     group    the active queries are counting-sorted by anchor; each gets a
+//              16-byte descriptor in anchor order.
+//     filter   (CTA per (anchor, half-row) work item): TMA copies the anchor's
+//              half rank row pos[a][*] (n bytes) and the descriptors of every
+//              query that drew it into shared memory; the warps share the
+//              queries' list segments (256 entries) and write the new alive
+//              bits: lo <= pos[a][j] < hi is exactly the searchsorted window
+//              test of search.py:77-79, 133-134.  Every anchor row is read
+//              from HBM once per phase.
+//     draw     (warp per query): |S'|, empty-intersection rollback
+//              (search.py:136-137), next anchor avail[k] (search.py:122-131)
+//              selected over the alive bits, exact d_a and its window.
 //   F    (warp per query): fp16-screened final scan of S u {prev} with exact
 //        FP64 re-check.
-// A query that does not fit (first ring > LIGHT_MAX, > BULK_U used anchors
-// still in S) is marked heavy and recomputed from scratch by K2, so results
-// never depend on the path taken.
+// A query that does not fit (first ring > LIGHT_MAX, > BULK_U used anchors) is
+// marked heavy and recomputed from scratch by K2, so results never depend on
+// the path taken.
 #pragma once
 
 #include "riann_kernels.cuh"
@@ -24,22 +33,28 @@
 namespace rb {
 
 constexpr int LIGHT_MAX = 16384;  // largest first ring handled by the bulk path (u16 entries)
-constexpr int BULK_U = 4;        // used anchors tracked per query
+constexpr int BULK_U = 8;        // used anchors tracked per query (prev + 7 draws at max_rings = 8)
 constexpr int COARSE = 64;       // coarse index stride of the sorted rows
-constexpr int PH_WARPS = 16;     // warps per ring-phase CTA
-constexpr int PH_CHUNK = 64;     // queries per ring-phase work item
+constexpr int FCAP = 256;        // query descriptors per filter stage
+constexpr int FW2 = 16;          // warps per filter CTA
+constexpr int LCAP = 16384;      // list entries staged per filter sub-chunk
+constexpr int FSEG = 256;        // list entries per final-scan fill round (8 per lane)
 
 enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
 
+// Per-query state.  The candidate list is fixed after P0: S is the set of
+// alive entries (bit set in bits[sel]) of the list at pool[s_off ..
+// s_off + lenA8 + lenB8), ascending; entries of part A (j < n/2) come first.
 struct __align__(16) QState {
     double d_prev;
-    int64_t s_off;            // candidate slot offset in the pool
+    int64_t s_off;            // multiple of 128 entries
     uint64_t sh, sl, ih, il;  // PCG64 state and increment
     int32_t cS, first, rings, status;
-    int32_t anchor, nu, rng_has, p_in;
+    int32_t lenA8, lenB8, nu, rng_has;
     uint32_t rng_buf;
-    int32_t tests, exact, pad;
-    int32_t u[BULK_U];
+    int32_t tests, exact, pin_pos;  // pin_pos: list position of prev (-1: not in the first ring)
+    int32_t sel, anchor, lo, hi;    // bits buffer holding S; drawn anchor and its window [lo, hi)
+    uint16_t up[BULK_U];            // list positions of the used anchors (search.py:120, 130)
 };
 
 struct BulkParams {
@@ -50,8 +65,9 @@ struct BulkParams {
     const uint16_t *sidx;
     const uint16_t *pos;     // rank rows: pos[a][sidx[a][k]] = k
     const float *coarse;     // coarse[a][b] = sdist[a][b*COARSE]
+    const float *coarse1;    // coarse1[a][k] = coarse[a][k*cs1] (k < 32; +inf past the row)
     int64_t n;
-    int ncoarse;
+    int ncoarse, cs1;
     const float *units;
     const int32_t *prev;
     int64_t Q;
@@ -64,10 +80,11 @@ struct BulkParams {
     int max_rings;
     int passes;
     QState *st;
-    uint16_t *pool;          // candidate slots (variable size, atomic allocation)
+    uint16_t *pool;          // fixed candidate lists (atomic allocation)
     unsigned long long *pool_top;
     int64_t pool_cap;
-    uint16_t *p0_spill;      // per P0 warp: 2 * LIGHT_MAX entries
+    uint8_t *bits0, *bits1;  // alive bits of the pool entries, double-buffered by phase
+    int32_t *kept;           // per query: entries kept by the current filter phase
     int32_t *active_in;      // queries whose anchor is pending (this phase)
     const int32_t *n_active_in;
     int32_t *active_out;     // next phase
@@ -76,9 +93,8 @@ struct BulkParams {
     int32_t *n_heavy;
     int32_t *counts;         // per anchor row (n + 1)
     int32_t *starts;         // exclusive scan of counts
-    int32_t *grouped;        // active queries grouped by anchor
-    int32_t *item_next;      // work-item counter
-    int32_t *seg_next;       // 16 segment counters (ring phase scheduling)
+    int4 *gdesc;             // per active query in anchor order: (g, s_off/128, lo | lenA8/8 << 17, hi | lenB8/8 << 17)
+    int32_t *item_next;      // filter work-item counter
     int32_t *out_idx;
     double *out_dist;
     unsigned long long *stats;
@@ -173,6 +189,19 @@ __device__ __forceinline__ void window_coarse(const float *__restrict__ row, con
     hi = __shfl_sync(FULL, res, 16);
 }
 
+// exact d_a (search.py:131, numpy order) and the anchor's window on its sorted
+// row (search.py:133 via :77-79), whole warp
+template <int D>
+__device__ __forceinline__ void anchor_window(const BulkParams &P, int a, const float *q, int lane, int &lo, int &hi)
+{
+    const double da = exact_dist_all<D>(P.refs, a, q, D, lane);
+    int64_t l, h;
+    window_coarse(P.sdist + (int64_t)a * P.n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, P.n,
+                  __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, l, h);
+    lo = (int)l;
+    hi = (int)h;
+}
+
 // k-th (0-based) element of ascending list S minus the used anchors u[0..nu)
 // (search.py:122, 129).  upos: positions of the used anchors in S.
 __device__ __forceinline__ int avail_pos(int k, const int *upos, int nu)
@@ -187,24 +216,44 @@ __device__ __forceinline__ int avail_pos(int k, const int *upos, int nu)
     return pos;
 }
 
-__device__ __forceinline__ int lower_bound_u16(const uint16_t *a, int cnt, uint32_t x)
+// List position of the k-th (0-based) alive entry that is not a used anchor
+// (avail[k], search.py:122, 129); bw: the query's alive-bit words, up/ua: used
+// anchor positions and which of them are alive.  Whole warp.
+__device__ __forceinline__ int select_avail(const uint32_t *bw, int nwords, const uint16_t (&up)[BULK_U], int nu,
+                                            int k, int lane)
 {
-    int lo = 0, hi = cnt;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if ((uint32_t)a[mid] < x) lo = mid + 1;
-        else hi = mid;
+    int run = 0;
+    for (int w0 = 0; w0 < nwords; w0 += 32) {
+        const int wi = w0 + lane;
+        uint32_t word = wi < nwords ? bw[wi] : 0u;
+#pragma unroll
+        for (int u = 0; u < BULK_U; u++)
+            if (u < nu && (up[u] >> 5) == wi) word &= ~(1u << (up[u] & 31));
+        const int c = __popc(word);
+        const int inc = warp_incl_scan(c, lane);
+        const int tot = __shfl_sync(FULL, inc, 31);
+        if (k < run + tot) {
+            const int ex = run + inc - c;
+            int pos = -1;
+            if (k >= ex && k < ex + c) pos = wi * 32 + (int)__fns(word, 0u, k - ex + 1);
+            const unsigned b = __ballot_sync(FULL, pos >= 0);
+            return __shfl_sync(FULL, pos, __ffs(b) - 1);
+        }
+        run += tot;
     }
-    return lo;
+    return -1;
 }
 
+__device__ __forceinline__ int bit_at(const uint8_t *bits, int64_t e) { return (bits[e >> 3] >> (e & 7)) & 1; }
+
 // ---------------------------------------------------------------------------
-// P0: first ring, candidate slot, first anchor.  One warp per query.
+// P0: first ring, fixed candidate list, first anchor.  One warp per query.
 // The first-ring window (unordered: distance order) becomes the ascending
 // candidate list (np.sort, search.py:116) through a per-warp n-bit bitmap in
-// shared memory, enumerated word-interleaved: at step t lane L takes word
-// 32t + L, a warp prefix sum places its bits, so each step's stores fall in
-// one short run of the slot.
+// shared memory, enumerated word-interleaved: at step t lane L takes words
+// 128t + 4L .. +3, a warp prefix sum places its bits, so each step's stores
+// fall in one short run of the slot.  Part B (j >= n/2) starts at the next
+// multiple of 8 after part A.
 __host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 4095) / 4096) * 128); }
 
 template <int D>
@@ -215,6 +264,7 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int64_t n = P.n;
+    const int jh = (int)(n >> 1);
     const int NW = p0_words(n);  // multiple of 128
     uint32_t *bm = smem_w + (size_t)wib * NW;
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
@@ -234,10 +284,11 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
         window_coarse(P.sdist + (int64_t)p * n, P.coarse + (int64_t)p * P.ncoarse, P.ncoarse, n,
                       __dsub_rn(d, __dmul_rn(P.alpha, d)), __dadd_rn(d, __dmul_rn(P.alpha, d)), lane, lo, hi);
         const int cS = (int)(hi - lo);
+        const int alloc = (cS + 14 + 127) & ~127;  // >= lenA8 + lenB8; bits of a list 16-byte aligned
         int64_t off = 0;
         if (lane == 0 && cS <= LIGHT_MAX) {
-            off = (int64_t)atomicAdd(P.pool_top, (unsigned long long)((cS + 7) & ~7));
-            if (off + cS > P.pool_cap) off = -1;
+            off = (int64_t)atomicAdd(P.pool_top, (unsigned long long)alloc);
+            if (off + alloc > P.pool_cap) off = -1;
         }
         off = __shfl_sync(FULL, off, 0);
         if (cS > LIGHT_MAX || off < 0) {
@@ -248,9 +299,13 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             continue;
         }
         // window of the u16 index row -> bitmap (16-byte vector loads on the aligned span)
+        int cA = 0;  // entries of part A (j < n/2)
         {
             const uint16_t *row = P.sidx + (int64_t)p * n;
-            auto mark = [&](uint32_t j) { atomicOr(&bm[j >> 5], 1u << (j & 31)); };
+            auto mark = [&](uint32_t j) {
+                atomicOr(&bm[j >> 5], 1u << (j & 31));
+                cA += (int)j < jh ? 1 : 0;
+            };
             const int64_t a0 = (lo + 7) & ~(int64_t)7, a1 = hi & ~(int64_t)7;
             if (a0 < a1) {
                 for (int64_t k = lo + lane; k < a0; k += 32) mark(__ldg(row + k));
@@ -265,6 +320,9 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
                 for (int64_t k = lo + lane; k < hi; k += 32) mark(__ldg(row + k));
             }
         }
+        cA = __reduce_add_sync(FULL, cA);
+        const int lenA8 = (cA + 7) & ~7, lenB8 = (cS - cA + 7) & ~7;
+        const int gap = lenA8 - cA;
         __syncwarp();
         // enumerate ascending into the slot, clearing the bitmap; rank and presence of p.
         // Step t: lane L takes words 128t + 4L .. +3 (one LDS.128); one warp scan per step.
@@ -288,7 +346,8 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
                 p_in = (wd[wp & 3] >> (p & 31)) & 1u;
             }
             if (any4) {
-                uint16_t *dst = slot + o;
+                bool crossed = w0 * 32 >= jh;
+                uint16_t *dst = slot + o + (crossed ? gap : 0);
                 const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
@@ -297,7 +356,12 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
                     while (word) {
                         const int b = __ffs(word) - 1;
                         word &= word - 1;
-                        *dst++ = (uint16_t)(base + b);
+                        const uint32_t j = base + b;
+                        if (!crossed && (int)j >= jh) {
+                            crossed = true;
+                            dst += gap;
+                        }
+                        *dst++ = (uint16_t)j;
                     }
                 }
             }
@@ -306,11 +370,40 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
         const int lp = (wp >> 2) & 31;
         below = __shfl_sync(FULL, below, lp);
         p_in = __shfl_sync(FULL, p_in, lp);
+        // alive bits of the list (both buffers zero past the list end, whole words)
+        {
+            const int nb = (lenA8 + lenB8) >> 3, nbw = alloc >> 3;
+            uint8_t *b0 = P.bits0 + (off >> 3), *b1 = P.bits1 + (off >> 3);
+            for (int b = lane; b < nbw; b += 32) {
+                uint8_t v = 0;
+                if (b < nb) {
+                    const int rem = b < (lenA8 >> 3) ? cA - 8 * b : (cS - cA) - 8 * (b - (lenA8 >> 3));
+                    v = rem >= 8 ? 0xffu : (uint8_t)((1u << rem) - 1u);
+                } else {
+                    b1[b] = 0;
+                }
+                b0[b] = v;
+            }
+        }
         __threadfence_block();
         __syncwarp();
+        // first anchor (search.py:119-131), drawn by lane 0
+        const bool loop = cS >= P.L && P.max_rings > 1 && cS - p_in > 0;
+        int an = -1, apos = -1;
+        Pcg64 rng;
+        if (lane == 0 && loop) {
+            seed_frame(rng, P, g);
+            int upos[1] = {below};
+            const int k = (int)pcg_integers(rng, (uint64_t)(cS - p_in));
+            const int r = avail_pos(k, upos, p_in);
+            apos = r + (r >= cA ? gap : 0);
+            an = (int)slot[apos];
+        }
+        an = __shfl_sync(FULL, an, 0);
+        int wlo = 0, whi = 0;
+        if (loop) anchor_window<D>(P, an, q, lane, wlo, whi);
         if (lane == 0) {
             QState s;
-            const bool loop = cS >= P.L && P.max_rings > 1;
             s.d_prev = d;
             s.s_off = off;
             s.cS = cS;
@@ -318,25 +411,25 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             s.rings = 1;
             s.tests = 0;
             s.exact = 1;
-            s.p_in = p_in;
+            s.lenA8 = lenA8;
+            s.lenB8 = lenB8;
+            s.pin_pos = p_in ? below + (p >= jh ? gap : 0) : -1;
+            s.sel = 0;
             s.nu = 0;
             s.rng_has = 0;
             s.rng_buf = 0;
             s.sh = s.sl = s.ih = s.il = 0;
             s.anchor = 0;
-            int upos[BULK_U];
-            if (p_in) {
-                s.u[0] = p;
-                upos[0] = below;
-                s.nu = 1;
-            }
-            if (loop && cS - s.nu > 0) {
-                Pcg64 rng;
-                seed_frame(rng, P, g);
-                const int k = (int)pcg_integers(rng, (uint64_t)(cS - s.nu));
-                const int pos = avail_pos(k, upos, s.nu);
-                s.anchor = (int)slot[pos];
-                s.u[s.nu++] = s.anchor;
+            s.lo = s.hi = 0;
+#pragma unroll
+            for (int k = 0; k < BULK_U; k++) s.up[k] = 0;
+            if (p_in) s.up[s.nu++] = (uint16_t)s.pin_pos;
+            if (loop) {
+                s.up[s.nu++] = (uint16_t)apos;
+                s.anchor = an;
+                s.lo = wlo;
+                s.hi = whi;
+                s.exact = 2;
                 rng_store(s, rng);
                 s.status = ST_ACTIVE;
                 P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
@@ -344,6 +437,7 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
                 s.status = ST_DONE;
             }
             P.st[g] = s;
+            P.kept[g] = 0;
         }
         __syncwarp();
     }
@@ -357,22 +451,20 @@ __global__ void bulk_count_kernel(BulkParams P)
         atomicAdd(P.counts + P.st[P.active_in[i]].anchor, 1);
 }
 
+// descriptors of the active queries in anchor order
 __global__ void bulk_scatter_kernel(BulkParams P)
 {
     const int m = *P.n_active_in;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const int g = P.active_in[i];
-        const int a = P.st[g].anchor;
-        P.grouped[P.starts[a] + atomicAdd(P.counts + a, 1)] = g;
+        const QState &s = P.st[g];
+        const int a = s.anchor;
+        P.gdesc[P.starts[a] + atomicAdd(P.counts + a, 1)] =
+            make_int4(g, (int)(s.s_off >> 7), s.lo | ((s.lenA8 >> 3) << 17), s.hi | ((s.lenB8 >> 3) << 17));
     }
 }
 
 // ---------------------------------------------------------------------------
-// Ring phase: CTA per work item (PH_CHUNK consecutive grouped queries).  For
-// each run of queries sharing an anchor, one thread starts a TMA bulk copy of
-// the anchor's rank row into shared memory; meanwhile every warp does its
-// queries' row-independent work (state, exact d_a, window search on the sorted
-// row); then the candidate lists are filtered against the shared row.
 __device__ __forceinline__ uint32_t smem_addr(const void *p)
 {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -410,144 +502,465 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigne
         : "memory");
 }
 
-// ---------------------------------------------------------------------------
-// Ring phase: one warp per (query, anchor), queries taken in anchor order so
-// the ~200 anchor rank rows in flight at any time stay resident in L2 (a row
-// is read from HBM about once per phase); membership tests are 8-deep
-// independent lookups pos[a][j] per lane.
-template <int D>
-__global__ void __launch_bounds__(256, 4) bulk_ring_kernel(BulkParams P)
+// next non-empty (anchor, half) work item of the filter phase
+__device__ __forceinline__ void filter_grab(const BulkParams &P, int &it, int &cnt, int &start)
 {
-    const int lane = threadIdx.x & 31;
-    const int64_t n = P.n;
-    const int m = *P.n_active_in;
-    // One entry per grab keeps the entries in flight GPU-wide -- and so the
-    // anchor rank rows that must stay L2-resident -- at one per resident warp.
-    // The anchor-ordered list is cut into NSEG segments with their own
-    // counters (atomic traffic / NSEG); a warp whose segment is exhausted
-    // steals from the next ones.
-    constexpr int NSEG = 16;
-    const int64_t gw0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int seg = (int)(gw0 % NSEG), tried = 0;
     for (;;) {
-        int i = -1;
-        if (lane == 0) {
-            while (tried < NSEG) {
-                const int s0 = (int)((int64_t)m * seg / NSEG), s1 = (int)((int64_t)m * (seg + 1) / NSEG);
-                const int t = s0 + atomicAdd(P.seg_next + seg, 1);
-                if (t < s1) {
-                    i = t;
-                    break;
-                }
-                seg = (seg + 1) % NSEG;
-                tried++;
-            }
+        const int i = atomicAdd(P.item_next, 1);
+        if (i >= 2 * P.n) {
+            it = -1;
+            return;
         }
-        i = __shfl_sync(FULL, i, 0);
-        if (i < 0) break;
-        const int64_t g = P.grouped[i];
-        QState *sp = P.st + g;
-        const int a = sp->anchor;
-        const int cS = sp->cS;
-        uint16_t *slot = P.pool + sp->s_off;
-        const float *q = P.units + g * D;
-        // search.py:131-133: exact d_a (numpy order), window on row a
-        const double da = exact_dist<D>(P.refs, a, q, D, lane % Lay<D>::G);
-        int64_t lo, hi;
-        window_coarse(P.sdist + (int64_t)a * n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, n,
-                      __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, lo, hi);
-        const uint16_t *prow = P.pos + (int64_t)a * n;
-        // search.py:134: S' = S n ring, order kept, filtered in place; per block of
-        // 1024 entries all list loads, then all rank lookups, are issued together
-        int nh = 0;
-        for (int base = 0; base < cS; base += 1024) {
-            uint4 v[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int i0 = base + k * 256 + lane * 8;
-                v[k] = i0 < cS ? *reinterpret_cast<const uint4 *>(slot + i0) : make_uint4(0, 0, 0, 0);
-            }
-            uint32_t keep4 = 0;  // 8 bits per k
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int i0 = base + k * 256 + lane * 8;
-                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
-                uint16_t pk[8];
-#pragma unroll
-                for (int x = 0; x < 8; x++) pk[x] = (i0 + x < cS) ? __ldg(prow + e8[x]) : (uint16_t)0xffff;
-#pragma unroll
-                for (int x = 0; x < 8; x++)
-                    if (i0 + x < cS && pk[x] >= lo && pk[x] < hi) keep4 |= 1u << (8 * k + x);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                if (base + k * 256 >= cS) break;
-                const unsigned keepm = (keep4 >> (8 * k)) & 0xffu;
-                const int kc = __popc(keepm);
-                const int inc = warp_incl_scan(kc, lane);
-                const int tot = __shfl_sync(FULL, inc, 31);
-                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
-                int o = nh + inc - kc;
-#pragma unroll
-                for (int x = 0; x < 8; x++)
-                    if ((keepm >> x) & 1u) slot[o++] = e8[x];
-                nh += tot;
-            }
-            __syncwarp();
+        const int c = P.counts[i >> 1];
+        if (c > 0) {
+            it = i;
+            cnt = c;
+            start = P.starts[i >> 1];
+            return;
         }
-        if (lane == 0) {
-            sp->tests += cS;
-            sp->exact += 1;
-            const int rings = sp->rings + 1;
-            sp->rings = rings;
-            int status = ST_DONE;  // nh == 0: search.py:136-137 rollback
-            if (nh > 0) {
-                sp->cS = nh;
-                int u[BULK_U];
-                int nu = 0;
-                const int nu0 = sp->nu;
-                for (int k = 0; k < nu0; k++) {
-                    const int uk = sp->u[k];
-                    const int pk = __ldg(prow + uk);
-                    if (pk >= lo && pk < hi) u[nu++] = uk;
-                }
-                bool pin = false;
-                for (int k = 0; k < nu; k++) pin |= u[k] == P.prev[g];
-                sp->p_in = pin;
-                if (nh >= P.L && rings < P.max_rings && nh - nu > 0) {
-                    int upos[BULK_U];
-                    for (int k = 0; k < nu; k++) upos[k] = lower_bound_u16(slot, nh, (uint32_t)u[k]);
-                    Pcg64 rng;
-                    rng.sh = sp->sh;
-                    rng.sl = sp->sl;
-                    rng.ih = sp->ih;
-                    rng.il = sp->il;
-                    rng.has = sp->rng_has;
-                    rng.buf = sp->rng_buf;
-                    const int k = (int)pcg_integers(rng, (uint64_t)(nh - nu));
-                    const int pos = avail_pos(k, upos, nu);
-                    if (nu >= BULK_U) {
-                        status = ST_HEAVY;
-                        P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
-                    } else {
-                        const int an = (int)slot[pos];
-                        sp->anchor = an;
-                        u[nu++] = an;
-                        sp->sh = rng.sh;
-                        sp->sl = rng.sl;
-                        sp->rng_has = rng.has;
-                        sp->rng_buf = rng.buf;
-                        status = ST_ACTIVE;
-                        P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Ring phase filter (search.py:133-134).  Work item (a, h): half h of anchor
+// a's rank row (entries j in [h n/2, (h+1) n/2), n bytes) plus the part-h list
+// ranges of the queries that drew a arrive in shared memory by TMA bulk copies
+// (one mbarrier); the staged 8-entry groups are spread evenly over all lanes,
+// each testing its alive entries: lo <= pos[a][j] < hi.  New alive bits go to
+// the other bit buffer, kept counts to kept[g].  The next item's descriptors
+// are fetched while the current copies fly; two CTAs per SM overlap one CTA's
+// copies with the other's filtering.
+__host__ __device__ constexpr size_t filter_smem(int64_t n)
+{
+    return (size_t)n + LCAP * 2 + 2 * FCAP * 16 + LCAP / 8 + (FCAP + 1) * 4 + FCAP * 4;
+}
+
+__global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, int cur)
+{
+    extern __shared__ __align__(128) unsigned char smem_f[];
+    constexpr int NPRE = LCAP / 8 / (FW2 * 32);  // staged groups per thread
+    const int64_t n = P.n;
+    const int jh = (int)(n >> 1);
+    uint16_t *row = reinterpret_cast<uint16_t *>(smem_f);
+    uint16_t *stage = reinterpret_cast<uint16_t *>(smem_f + n);
+    int4 *descb = reinterpret_cast<int4 *>(smem_f + n + LCAP * 2);
+    uint8_t *gmap = reinterpret_cast<uint8_t *>(descb + 2 * FCAP);
+    int *qg0 = reinterpret_cast<int *>(gmap + LCAP / 8);
+    int *kept_s = qg0 + FCAP + 1;
+    __shared__ uint64_t dbar[2], rbar;
+    __shared__ int s_it[2], s_cnt[2], s_start[2], s_q1, s_ng;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint8_t *bcur = cur ? P.bits1 : P.bits0;
+    uint8_t *bnxt = cur ? P.bits0 : P.bits1;
+    auto fetch_desc = [&](int b, int start, int m) {  // one thread
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&dbar[b], (unsigned)m * 16u);
+        tma_bulk_g2s(descb + b * FCAP, P.gdesc + start, (unsigned)m * 16u, &dbar[b]);
+    };
+    if (tid == 0) {
+        mbar_init(&dbar[0], 1);
+        mbar_init(&dbar[1], 1);
+        mbar_init(&rbar, 1);
+        int it, cnt = 0, start = 0;
+        filter_grab(P, it, cnt, start);
+        s_it[0] = it;
+        s_cnt[0] = cnt;
+        s_start[0] = start;
+        if (it >= 0) fetch_desc(0, start, min(cnt, FCAP));
+    }
+    for (int i = tid; i < FCAP; i += blockDim.x) kept_s[i] = 0;
+    __syncthreads();
+    unsigned dpar0 = 0, dpar1 = 0, rpar = 0;
+    int db = 0;
+    for (;;) {
+        const int it = s_it[db];
+        if (it < 0) break;
+        const int cnt = s_cnt[db], start = s_start[db];
+        const int a = it >> 1, h = it & 1;
+        int4 *desc = descb + db * FCAP;
+        bool first_sub = true;
+        for (int c0 = 0; c0 < cnt; c0 += FCAP) {
+            const int m = min(FCAP, cnt - c0);
+            if (c0 > 0 && tid == 0) fetch_desc(db, start + c0, m);
+            if (db == 0) {
+                mbar_wait(&dbar[0], dpar0);
+                dpar0 ^= 1;
+            } else {
+                mbar_wait(&dbar[1], dpar1);
+                dpar1 ^= 1;
+            }
+            for (int q0 = 0; q0 < m;) {
+                // warp 0: sub-chunk [q0, q1) whose part-h lists fit the staging
+                // buffer, their staged group offsets, and the copies
+                if (w == 0) {
+                    int run = 0, q1 = q0;
+                    for (int b = q0; b < m; b += 32) {
+                        const int i = b + lane;
+                        int ng = 0;
+                        if (i < m) {
+                            const int4 d = desc[i];
+                            ng = h ? (d.w >> 17) : (d.z >> 17);
+                        }
+                        const int inc = warp_incl_scan(ng, lane);
+                        const bool fits = i < m && (run + inc) * 8 <= LCAP;
+                        const int nf = __popc(__ballot_sync(FULL, fits));
+                        if (fits) qg0[i - q0] = run + inc - ng;
+                        if (nf > 0) run += __shfl_sync(FULL, inc, nf - 1);
+                        q1 = b + nf;
+                        if (nf < 32) break;
+                    }
+                    if (lane == 0) {
+                        qg0[q1 - q0] = run;
+                        s_q1 = q1;
+                        s_ng = run;
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        mbar_expect_tx(&rbar, (unsigned)run * 16u + (first_sub ? (unsigned)n : 0u));
+                        if (first_sub)
+                            tma_bulk_g2s(row, P.pos + (int64_t)a * n + (int64_t)h * jh, (unsigned)n, &rbar);
+                    }
+                    __syncwarp();
+                    for (int i = q0 + lane; i < q1; i += 32) {
+                        const int4 d = desc[i];
+                        const int ng = h ? (d.w >> 17) : (d.z >> 17);
+                        if (ng > 0) {
+                            const int64_t src = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0);
+                            tma_bulk_g2s(stage + (int64_t)qg0[i - q0] * 8, P.pool + src, (unsigned)ng * 16u, &rbar);
+                        }
                     }
                 }
-                for (int k = 0; k < nu; k++) sp->u[k] = u[k];
-                sp->nu = nu;
+                __syncthreads();
+                const int q1 = s_q1, NG = s_ng, mq = q1 - q0;
+                for (int i = w; i < mq; i += FW2) {
+                    const int g0 = qg0[i], g1 = qg0[i + 1];
+                    for (int x = g0 + lane; x < g1; x += 32) gmap[x] = (uint8_t)i;
+                }
+                __syncthreads();
+                // alive bytes of my groups (independent of the copies)
+                uint32_t al[NPRE];
+                int qi[NPRE];
+                int64_t eb[NPRE];
+#pragma unroll
+                for (int k = 0; k < NPRE; k++) {
+                    const int G = k * FW2 * 32 + tid;
+                    qi[k] = -1;
+                    al[k] = 0;
+                    eb[k] = 0;
+                    if (G < NG) {
+                        const int x = gmap[G];
+                        const int4 d = desc[q0 + x];
+                        qi[k] = x;
+                        eb[k] = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0) + (int64_t)(G - qg0[x]) * 8;
+                        al[k] = bcur[eb[k] >> 3];
+                    }
+                }
+                // the next item and its descriptors, while the copies fly
+                if (first_sub && c0 == 0 && w == 1 && lane == 0) {
+                    int nit, ncnt = 0, nstart = 0;
+                    filter_grab(P, nit, ncnt, nstart);
+                    s_it[db ^ 1] = nit;
+                    s_cnt[db ^ 1] = ncnt;
+                    s_start[db ^ 1] = nstart;
+                    if (nit >= 0) fetch_desc(db ^ 1, nstart, min(ncnt, FCAP));
+                }
+                mbar_wait(&rbar, rpar);
+                rpar ^= 1;
+                const uint16_t *rowb = row - (int64_t)h * jh;  // indexed by j
+#pragma unroll
+                for (int k = 0; k < NPRE; k++) {
+                    if (k * FW2 * 32 >= NG) break;  // block-uniform
+                    const int G = k * FW2 * 32 + tid;
+                    uint32_t keep = 0;
+                    if (qi[k] >= 0) {
+                        const int4 d = desc[q0 + qi[k]];
+                        const int lo = d.z & 0x1ffff, hi = d.w & 0x1ffff;
+                        const uint4 v = *reinterpret_cast<const uint4 *>(stage + (int64_t)G * 8);
+                        const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
+#pragma unroll
+                        for (int x = 0; x < 8; x++) {
+                            if ((al[k] >> x) & 1u) {
+                                const int r = rowb[e8[x]];
+                                if (r >= lo && r < hi) keep |= 1u << x;
+                            }
+                        }
+                        bnxt[eb[k] >> 3] = (uint8_t)keep;
+                    }
+                    const int q_l0 = __shfl_sync(FULL, qi[k], 0);
+                    const int c = __popc(keep);
+                    if (__all_sync(FULL, qi[k] == q_l0)) {
+                        const int cw = __reduce_add_sync(FULL, c);
+                        if (lane == 0 && q_l0 >= 0 && cw > 0) atomicAdd(&kept_s[q_l0], cw);
+                    } else if (qi[k] >= 0 && c > 0) {
+                        atomicAdd(&kept_s[qi[k]], c);
+                    }
+                }
+                __syncthreads();
+                for (int i = tid; i < mq; i += blockDim.x) {
+                    const int c = kept_s[i];
+                    if (c > 0) {
+                        atomicAdd(P.kept + desc[q0 + i].x, c);
+                        kept_s[i] = 0;
+                    }
+                }
+                first_sub = false;
+                q0 = q1;
+                __syncthreads();
+            }
+        }
+        db ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Ring phase draw (search.py:121-137): four queries per warp, eight lanes each.
+// |S'| = kept, rollback on an empty intersection, next anchor avail[k] from the
+// query's generator (select over the alive bits), its exact distance (numpy
+// order: lane j holds accumulator j of each 96/64-element half) and its window
+// on the sorted row in three rounds: 32-entry level-1 index, 32 coarse entries,
+// <= 64 row values.
+template <int D>
+__device__ __forceinline__ double dist8(const float *__restrict__ r, const float (&qv)[D / 8], int gl)
+{
+    constexpr int H = D > 128 ? D / 2 : D;  // numpy pairwise halves
+    constexpr int PER = H / 8;
+    double h0 = sqdiff(__ldg(r + gl), qv[0]);
+#pragma unroll
+    for (int i = 1; i < PER; i++) h0 = __dadd_rn(h0, sqdiff(__ldg(r + gl + 8 * i), qv[i]));
+    double h1 = 0.0;
+    if constexpr (D > 128) {
+        h1 = sqdiff(__ldg(r + H + gl), qv[PER]);
+#pragma unroll
+        for (int i = 1; i < PER; i++) h1 = __dadd_rn(h1, sqdiff(__ldg(r + H + gl + 8 * i), qv[PER + i]));
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        h0 = __dadd_rn(h0, __shfl_xor_sync(FULL, h0, o));
+        if constexpr (D > 128) h1 = __dadd_rn(h1, __shfl_xor_sync(FULL, h1, o));
+    }
+    if constexpr (D > 128) h0 = __dadd_rn(h0, h1);
+    return __dsqrt_rn(h0);
+}
+
+__device__ __forceinline__ int grp_sum(int v)
+{
+    v += __shfl_xor_sync(FULL, v, 1);
+    v += __shfl_xor_sync(FULL, v, 2);
+    v += __shfl_xor_sync(FULL, v, 4);
+    return v;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur)
+{
+    static_assert(D % 8 == 0 && D <= 256, "draw kernel dims");
+    const int lane = threadIdx.x & 31, gl = lane & 7, gb = lane & ~7;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t n = P.n;
+    const int nb = P.ncoarse, cs1 = P.cs1;
+    const uint8_t *bnxt = cur ? P.bits0 : P.bits1;
+    constexpr int HD = D > 128 ? D / 2 : D;
+    // queries in index order (the state, unit rows, lists and bits then stream
+    // sequentially); those filtered this phase have status ACTIVE
+    for (int64_t ib = gwarp * 4; ib < P.Q; ib += nwarps * 4) {
+        const int64_t gi = ib + (lane >> 3);
+        const int64_t g = gi < P.Q ? gi : 0;
+        QState *sp = P.st + g;
+        // the whole state: lane gl holds bytes 16 gl .. 16 gl + 15
+        uint4 sv = gi < P.Q ? reinterpret_cast<const uint4 *>(sp)[gl] : make_uint4(0u, 0u, 0u, 0u);
+        const bool has = __shfl_sync(FULL, sv.w, gb | 3) == (uint32_t)ST_ACTIVE && gi < P.Q;  // word 15: status
+        if (!has) sv = make_uint4(0u, 0u, 0u, 0u);
+        if (!__any_sync(FULL, has)) continue;
+        const int kept = has ? P.kept[g] : 0;
+        float qv[D / 8];
+        {
+            const float *q = P.units + g * D;
+#pragma unroll
+            for (int k = 0; k < HD / 8; k++) qv[k] = __ldg(q + gl + 8 * k);
+            if constexpr (D > 128) {
+#pragma unroll
+                for (int k = 0; k < HD / 8; k++) qv[HD / 8 + k] = __ldg(q + HD + gl + 8 * k);
+            }
+        }
+        auto word = [&](int wi) {  // 32-bit word wi of the state (compile-time wi)
+            const uint32_t c = (wi & 3) == 0 ? sv.x : (wi & 3) == 1 ? sv.y : (wi & 3) == 2 ? sv.z : sv.w;
+            return __shfl_sync(FULL, c, gb | (wi >> 2));
+        };
+        const int64_t soff = (int64_t)((uint64_t)word(2) | ((uint64_t)word(3) << 32));
+        const int cS = (int)word(12);
+        const int rings = (int)word(14) + 1;
+        const int W = (int)word(16) + (int)word(17);
+        const int nu = (int)word(18);
+        uint16_t up[BULK_U];
+        {
+            const uint32_t u0 = word(28), u1 = word(29), u2 = word(30), u3 = word(31);
+            up[0] = (uint16_t)u0; up[1] = (uint16_t)(u0 >> 16);
+            up[2] = (uint16_t)u1; up[3] = (uint16_t)(u1 >> 16);
+            up[4] = (uint16_t)u2; up[5] = (uint16_t)(u2 >> 16);
+            up[6] = (uint16_t)u3; up[7] = (uint16_t)(u3 >> 16);
+        }
+        const uint8_t *bq = bnxt + (soff >> 3);
+        int ub = 0;
+        if (kept > 0 && gl < nu) ub = bit_at(bq, up[gl]);
+        const int nua = grp_sum(ub);
+        const bool want = kept > 0 && kept >= P.L && rings < P.max_rings && kept - nua > 0;
+        const bool drew = want && nu < BULK_U;
+        // numpy Generator.integers(|avail|) by the group's lane 0
+        Pcg64 rng;
+        rng.sh = (uint64_t)word(4) | ((uint64_t)word(5) << 32);
+        rng.sl = (uint64_t)word(6) | ((uint64_t)word(7) << 32);
+        rng.ih = (uint64_t)word(8) | ((uint64_t)word(9) << 32);
+        rng.il = (uint64_t)word(10) | ((uint64_t)word(11) << 32);
+        rng.has = (int)word(19);
+        rng.buf = word(20);
+        int kk = 0;
+        if (drew && gl == 0) kk = (int)pcg_integers(rng, (uint64_t)(kept - nua));
+        kk = __shfl_sync(FULL, kk, gb);
+        // avail[kk]: 32 bit words per round, 4 per lane
+        int apos = -1;
+        {
+            const int nw = drew ? (W + 31) >> 5 : 0;
+            int rounds = (nw + 31) >> 5;
+            rounds = __reduce_max_sync(FULL, rounds);
+            int run = 0;
+            for (int r = 0; r < rounds; r++) {
+                const int w0 = r * 32 + gl * 4;
+                uint32_t wd[4] = {0u, 0u, 0u, 0u};
+                if (w0 < nw) {
+                    const uint4 b4 = *reinterpret_cast<const uint4 *>(bq + (int64_t)w0 * 4);
+                    wd[0] = b4.x;
+                    wd[1] = b4.y;
+                    wd[2] = b4.z;
+                    wd[3] = b4.w;
+                }
+#pragma unroll
+                for (int u = 0; u < BULK_U; u++) {
+                    const int wu = (int)(up[u] >> 5) - w0;
+                    if (u < nu && wu >= 0 && wu < 4) {
+#pragma unroll
+                        for (int x = 0; x < 4; x++)
+                            if (x == wu) wd[x] &= ~(1u << (up[u] & 31));
+                    }
+                }
+                const int c = __popc(wd[0]) + __popc(wd[1]) + __popc(wd[2]) + __popc(wd[3]);
+                int inc = c;
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    const int t = __shfl_up_sync(FULL, inc, o);
+                    if (gl >= o) inc += t;
+                }
+                const int tot = __shfl_sync(FULL, inc, gb | 7);
+                const int ex = run + inc - c;
+                if (apos < 0 && kk >= ex && kk < ex + c) {
+                    int kr = kk - ex;
+#pragma unroll
+                    for (int x = 0; x < 4; x++) {
+                        const int cx = __popc(wd[x]);
+                        if (kr >= 0 && kr < cx) apos = (w0 + x) * 32 + (int)__fns(wd[x], 0u, kr + 1);
+                        kr -= cx;
+                    }
+                }
+                run += tot;
+            }
+            // broadcast within the group
+            const unsigned bal = __ballot_sync(FULL, apos >= 0) & (0xffu << gb);
+            apos = __shfl_sync(FULL, apos, bal ? __ffs(bal) - 1 : gb);
+            if (!drew) apos = -1;
+        }
+        int an = 0;
+        if (drew && gl == 0) an = (int)P.pool[soff + apos];
+        an = __shfl_sync(FULL, an, gb);
+        // exact d_a + level-1 row (one round)
+        float4 l1 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (drew) l1 = __ldg(reinterpret_cast<const float4 *>(P.coarse1 + (int64_t)an * 32) + gl);
+        const double da = dist8<D>(P.refs + (int64_t)an * D, qv, gl);
+        const double lv = __dsub_rn(da, __dmul_rn(P.alpha, da)), hv = __dadd_rn(da, __dmul_rn(P.alpha, da));
+        int b1lo, b1hi;
+        {
+            const float e[4] = {l1.x, l1.y, l1.z, l1.w};
+            int cl = 0, ch = 0;
+#pragma unroll
+            for (int x = 0; x < 4; x++) {
+                cl += (double)e[x] < lv ? 1 : 0;
+                ch += (double)e[x] <= hv ? 1 : 0;
+            }
+            b1lo = grp_sum(cl);
+            b1hi = grp_sum(ch);
+        }
+        // coarse round: lanes 0-3 of the group for lo, 4-7 for hi
+        const bool sh = gl >= 4;
+        const int sl = gl & 3;
+        const double thr = sh ? hv : lv;
+        int b;
+        {
+            const int b1 = sh ? b1hi : b1lo;
+            int cnt = 0;
+            const int cb = (b1 - 1) * cs1;
+            if (drew && b1 > 0) {
+                const int cend = min(b1 * cs1, nb);
+                const float *cr = P.coarse + (int64_t)an * nb;
+#pragma unroll
+                for (int x = 0; x < 8; x++) {
+                    const int ci = cb + 1 + sl * 8 + x;
+                    if (ci < cend) {
+                        const double v = (double)__ldg(cr + ci);
+                        cnt += (sh ? v <= thr : v < thr) ? 1 : 0;
+                    }
+                }
+            }
+            cnt += __shfl_xor_sync(FULL, cnt, 1);
+            cnt += __shfl_xor_sync(FULL, cnt, 2);
+            b = b1 > 0 ? cb + 1 + cnt : 0;
+        }
+        // fine round: <= 63 row values
+        int res;
+        {
+            const int64_t s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
+            const int64_t s1 = b < nb ? (int64_t)b * COARSE : n;
+            int cnt = 0;
+            if (drew) {
+                const float *rr = P.sdist + (int64_t)an * n;
+#pragma unroll
+                for (int x = 0; x < 16; x++) {
+                    const int64_t k = s0 + sl * 16 + x;
+                    if (k < s1) {
+                        const double v = (double)__ldg(rr + k);
+                        cnt += (sh ? v <= thr : v < thr) ? 1 : 0;
+                    }
+                }
+            }
+            cnt += __shfl_xor_sync(FULL, cnt, 1);
+            cnt += __shfl_xor_sync(FULL, cnt, 2);
+            res = (int)(s0 + cnt);
+        }
+        const int wlo = __shfl_sync(FULL, res, gb), whi = __shfl_sync(FULL, res, gb | 4);
+        if (has && gl == 0) {
+            sp->tests += cS;
+            sp->rings = rings;
+            P.kept[g] = 0;
+            int status = ST_DONE;
+            if (kept > 0) {
+                sp->cS = kept;
+                sp->sel = cur ^ 1;
+            }
+            if (drew) {
+                sp->exact += 1;
+                sp->anchor = an;
+                sp->lo = wlo;
+                sp->hi = whi;
+                sp->up[nu] = (uint16_t)apos;
+                sp->nu = nu + 1;
+                sp->sh = rng.sh;
+                sp->sl = rng.sl;
+                sp->rng_has = rng.has;
+                sp->rng_buf = rng.buf;
+                status = ST_ACTIVE;
+                P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+            } else if (want) {
+                status = ST_HEAVY;
+                P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
             }
             sp->status = status;
         }
-        __syncwarp();
     }
 }
 
@@ -606,6 +1019,9 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
         const float *q = P.units + g * D;
         const float *qp = SP.units_pca + g * D;
         const uint16_t *slot = P.pool + sr.s_off;
+        const uint8_t *bq = (sr.sel ? P.bits1 : P.bits0) + (sr.s_off >> 3);
+        const int Wl = sr.lenA8 + sr.lenB8;
+        const bool p_in = sr.pin_pos >= 0 && bit_at(bq, sr.pin_pos);
         double bd = d;
         int bi = p;
         long long exact_cnt = sr.exact;
@@ -646,8 +1062,29 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
             return __fdiv_ru(__fmul_ru(r, r), 0.99997f);
         };
         float thr = thr_of(ub);
-        for (int blk = 0; blk < cS; blk += FB) {
-            const int bn = min(FB, cS - blk);
+        for (int lp = 0; lp < Wl;) {
+            // S = the alive list entries: up to FB of them into Bj's space
+            uint32_t *Cj = Bj;
+            int bn = 0;
+            while (lp < Wl && bn <= FB - FSEG) {
+                const int e0 = lp + lane * 8;
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                uint32_t al = 0;
+                if (e0 < Wl) {
+                    v = *reinterpret_cast<const uint4 *>(slot + e0);
+                    al = bq[e0 >> 3];
+                }
+                const int c = __popc(al);
+                const int inc = warp_incl_scan(c, lane);
+                int o = bn + inc - c;
+                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
+#pragma unroll
+                for (int x = 0; x < 8; x++)
+                    if ((al >> x) & 1u) Cj[o++] = e8[x];
+                bn += __shfl_sync(FULL, inc, 31);
+                lp += FSEG;
+            }
+            __syncwarp();
             // chunk 0 over the block, one candidate per lane
             float qc[16];
             {
@@ -665,7 +1102,7 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
             for (int e0 = 0; e0 < bn; e0 += 32) {
                 const int e = e0 + lane;
                 const bool valid = e < bn;
-                const uint32_t j = slot[blk + (valid ? e : 0)];
+                const uint32_t j = Cj[valid ? e : 0];
                 const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D);
                 const uint4 v0 = ld_keep16(rp, pol_keep), v1 = ld_keep16(rp + 1, pol_keep);
                 float s = 0.f;
@@ -780,7 +1217,7 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
         }
         flush();
         warp_argmin(bd, bi);
-        const int nscan = cS + (sr.p_in ? 0 : 1);
+        const int nscan = cS + (p_in ? 0 : 1);
         if (lane == 0) {
             P.out_idx[g] = bi;
             P.out_dist[g] = bd;
@@ -841,6 +1278,16 @@ __global__ void coarse_kernel(const float *sdist, int64_t n, int nb, float *coar
     if (i >= n * nb) return;
     int64_t a = i / nb, b = i - a * nb;
     coarse[i] = sdist[a * n + b * COARSE];
+}
+
+// level-1 index of the coarse rows: 32 entries per row, +inf past the row
+__global__ void coarse1_kernel(const float *coarse, int64_t n, int nb, int cs1, float *c1)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * 32) return;
+    int64_t a = i >> 5;
+    int k = (int)(i & 31);
+    c1[i] = (int64_t)k * cs1 < nb ? coarse[a * nb + (int64_t)k * cs1] : __int_as_float(0x7f800000);
 }
 
 }  // namespace rb

@@ -532,7 +532,7 @@ __device__ __forceinline__ void filter_grab(const BulkParams &P, int &it, int &c
 // copies with the other's filtering.
 __host__ __device__ constexpr size_t filter_smem(int64_t n)
 {
-    return (size_t)n + LCAP * 2 + 2 * FCAP * 16 + LCAP / 8 + (FCAP + 1) * 4 + FCAP * 4;
+    return (size_t)n + LCAP * 2 + 2 * FCAP * 16 + (FCAP + 1) * 4;
 }
 
 __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, int cur)
@@ -544,9 +544,7 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
     uint16_t *row = reinterpret_cast<uint16_t *>(smem_f);
     uint16_t *stage = reinterpret_cast<uint16_t *>(smem_f + n);
     int4 *descb = reinterpret_cast<int4 *>(smem_f + n + LCAP * 2);
-    uint8_t *gmap = reinterpret_cast<uint8_t *>(descb + 2 * FCAP);
-    int *qg0 = reinterpret_cast<int *>(gmap + LCAP / 8);
-    int *kept_s = qg0 + FCAP + 1;
+    int *qg0 = reinterpret_cast<int *>(descb + 2 * FCAP);
     __shared__ uint64_t dbar[2], rbar;
     __shared__ int s_it[2], s_cnt[2], s_start[2], s_q1, s_ng;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -568,7 +566,6 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
         s_start[0] = start;
         if (it >= 0) fetch_desc(0, start, min(cnt, FCAP));
     }
-    for (int i = tid; i < FCAP; i += blockDim.x) kept_s[i] = 0;
     __syncthreads();
     unsigned dpar0 = 0, dpar1 = 0, rpar = 0;
     int db = 0;
@@ -630,11 +627,6 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                 }
                 __syncthreads();
                 const int q1 = s_q1, NG = s_ng, mq = q1 - q0;
-                for (int i = w; i < mq; i += FW2) {
-                    const int g0 = qg0[i], g1 = qg0[i + 1];
-                    for (int x = g0 + lane; x < g1; x += 32) gmap[x] = (uint8_t)i;
-                }
-                __syncthreads();
                 // alive bytes of my groups (independent of the copies)
                 uint32_t al[NPRE];
                 int qi[NPRE];
@@ -646,7 +638,12 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                     al[k] = 0;
                     eb[k] = 0;
                     if (G < NG) {
-                        const int x = gmap[G];
+                        int x = 0, r = mq;  // last query with qg0 <= G
+                        while (r - x > 1) {
+                            const int mid = (x + r) >> 1;
+                            if (qg0[mid] <= G) x = mid;
+                            else r = mid;
+                        }
                         const int4 d = desc[q0 + x];
                         qi[k] = x;
                         eb[k] = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0) + (int64_t)(G - qg0[x]) * 8;
@@ -670,8 +667,10 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                     if (k * FW2 * 32 >= NG) break;  // block-uniform
                     const int G = k * FW2 * 32 + tid;
                     uint32_t keep = 0;
+                    int gq = -1;
                     if (qi[k] >= 0) {
                         const int4 d = desc[q0 + qi[k]];
+                        gq = d.x;
                         const int lo = d.z & 0x1ffff, hi = d.w & 0x1ffff;
                         const uint4 v = *reinterpret_cast<const uint4 *>(stage + (int64_t)G * 8);
                         const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
@@ -688,17 +687,9 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                     const int c = __popc(keep);
                     if (__all_sync(FULL, qi[k] == q_l0)) {
                         const int cw = __reduce_add_sync(FULL, c);
-                        if (lane == 0 && q_l0 >= 0 && cw > 0) atomicAdd(&kept_s[q_l0], cw);
+                        if (lane == 0 && q_l0 >= 0 && cw > 0) atomicAdd(P.kept + gq, cw);
                     } else if (qi[k] >= 0 && c > 0) {
-                        atomicAdd(&kept_s[qi[k]], c);
-                    }
-                }
-                __syncthreads();
-                for (int i = tid; i < mq; i += blockDim.x) {
-                    const int c = kept_s[i];
-                    if (c > 0) {
-                        atomicAdd(P.kept + desc[q0 + i].x, c);
-                        kept_s[i] = 0;
+                        atomicAdd(P.kept + gq, c);
                     }
                 }
                 first_sub = false;

@@ -1076,91 +1076,78 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
                 lp += FSEG;
             }
             __syncwarp();
-            // chunk 0 over the block, one candidate per lane
-            float qc[16];
+            // chunk 0 over the block: a lane pair per candidate, each lane one
+            // 16-byte half of its 32-byte chunk (one L1 wavefront per candidate)
+            const int hh = lane & 1;
+            const unsigned EVEN = 0x55555555u;
+            float qc[8];
             {
-                const float4 *q4 = reinterpret_cast<const float4 *>(qp);
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const float4 v = __ldg(q4 + k);
-                    qc[4 * k] = v.x;
-                    qc[4 * k + 1] = v.y;
-                    qc[4 * k + 2] = v.z;
-                    qc[4 * k + 3] = v.w;
-                }
+                const float4 *q4 = reinterpret_cast<const float4 *>(qp) + 2 * hh;
+                const float4 va = __ldg(q4), vb = __ldg(q4 + 1);
+                qc[0] = va.x; qc[1] = va.y; qc[2] = va.z; qc[3] = va.w;
+                qc[4] = vb.x; qc[5] = vb.y; qc[6] = vb.z; qc[7] = vb.w;
             }
-            int nA = 0;
-            for (int e0 = 0; e0 < bn; e0 += 32) {
-                const int e = e0 + lane;
-                const bool valid = e < bn;
-                const uint32_t j = Cj[valid ? e : 0];
-                const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D);
-                const uint4 v0 = ld_keep16(rp, pol_keep), v1 = ld_keep16(rp + 1, pol_keep);
+            auto part = [&](const uint4 &v) {
                 float s = 0.f;
-                const __half2 *h0 = reinterpret_cast<const __half2 *>(&v0);
-                const __half2 *h1 = reinterpret_cast<const __half2 *>(&v1);
+                const __half2 *h2 = reinterpret_cast<const __half2 *>(&v);
 #pragma unroll
                 for (int x = 0; x < 4; x++) {
-                    float2 f = __half22float2(h0[x]);
-                    float a0 = __fsub_rn(f.x, qc[2 * x]), a1 = __fsub_rn(f.y, qc[2 * x + 1]);
-                    s = __fmaf_rn(a0, a0, s);
-                    s = __fmaf_rn(a1, a1, s);
-                    f = __half22float2(h1[x]);
-                    a0 = __fsub_rn(f.x, qc[8 + 2 * x]);
-                    a1 = __fsub_rn(f.y, qc[8 + 2 * x + 1]);
+                    const float2 f = __half22float2(h2[x]);
+                    const float a0 = __fsub_rn(f.x, qc[2 * x]), a1 = __fsub_rn(f.y, qc[2 * x + 1]);
                     s = __fmaf_rn(a0, a0, s);
                     s = __fmaf_rn(a1, a1, s);
                 }
-                const bool keep = valid && s <= thr;
-                const unsigned ball = __ballot_sync(FULL, keep);
-                if (keep) {
-                    const int o = nA + __popc(ball & lanemask_lt());
-                    Aj[o] = j;
-                    As[o] = s;
+                return __fadd_rn(s, __shfl_xor_sync(FULL, s, 1));
+            };
+            int nA = 0;
+            // FU rounds of 16 candidates per iteration, their loads issued together
+            constexpr int FU = 4;
+            for (int e0 = 0; e0 < bn; e0 += 16 * FU) {
+                uint4 v[FU];
+                uint32_t jj[FU];
+#pragma unroll
+                for (int u = 0; u < FU; u++) {
+                    const int e = e0 + 16 * u + (lane >> 1);
+                    jj[u] = Cj[e < bn ? e : 0];
+                    v[u] = ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)jj[u] * D) + hh, pol_keep);
                 }
-                nA += __popc(ball);
+#pragma unroll
+                for (int u = 0; u < FU; u++) {
+                    const int e = e0 + 16 * u + (lane >> 1);
+                    const float s = part(v[u]);
+                    const bool keep = e < bn && s <= thr;
+                    const unsigned ball = __ballot_sync(FULL, keep) & EVEN;
+                    if (keep && hh == 0) {
+                        const int o = nA + __popc(ball & lanemask_lt());
+                        Aj[o] = jj[u];
+                        As[o] = s;
+                    }
+                    nA += __popc(ball);
+                }
             }
             __syncwarp();
             // further chunks for the candidates still alive
             for (int c = 1; c < NCH && nA > 0; c++) {
                 {
-                    const float4 *q4 = reinterpret_cast<const float4 *>(qp + 16 * c);
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const float4 v = __ldg(q4 + k);
-                        qc[4 * k] = v.x;
-                        qc[4 * k + 1] = v.y;
-                        qc[4 * k + 2] = v.z;
-                        qc[4 * k + 3] = v.w;
-                    }
+                    const float4 *q4 = reinterpret_cast<const float4 *>(qp + 16 * c) + 2 * hh;
+                    const float4 va = __ldg(q4), vb = __ldg(q4 + 1);
+                    qc[0] = va.x; qc[1] = va.y; qc[2] = va.z; qc[3] = va.w;
+                    qc[4] = vb.x; qc[5] = vb.y; qc[6] = vb.z; qc[7] = vb.w;
                 }
                 const bool last = c == NCH - 1;
                 int nB = 0;
-                for (int i0 = 0; i0 < nA; i0 += 32) {
-                    const int i = i0 + lane;
+                for (int i0 = 0; i0 < nA; i0 += 16) {
+                    const int i = i0 + (lane >> 1);
                     const bool valid = i < nA;
                     const uint32_t j = valid ? Aj[i] : Aj[0];
-                    float s = valid ? As[i] : 0.f;
-                    const uint4 *rp = reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D) + 2 * c;
-                    const uint4 v0 = ld_keep16(rp, pol_keep), v1 = ld_keep16(rp + 1, pol_keep);
-                    const __half2 *h0 = reinterpret_cast<const __half2 *>(&v0);
-                    const __half2 *h1 = reinterpret_cast<const __half2 *>(&v1);
-#pragma unroll
-                    for (int x = 0; x < 4; x++) {
-                        float2 f = __half22float2(h0[x]);
-                        float a0 = __fsub_rn(f.x, qc[2 * x]), a1 = __fsub_rn(f.y, qc[2 * x + 1]);
-                        s = __fmaf_rn(a0, a0, s);
-                        s = __fmaf_rn(a1, a1, s);
-                        f = __half22float2(h1[x]);
-                        a0 = __fsub_rn(f.x, qc[8 + 2 * x]);
-                        a1 = __fsub_rn(f.y, qc[8 + 2 * x + 1]);
-                        s = __fmaf_rn(a0, a0, s);
-                        s = __fmaf_rn(a1, a1, s);
-                    }
+                    const float s0 = valid ? As[i] : 0.f;
+                    const uint4 v =
+                        ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D) + 2 * c + hh, pol_keep);
+                    const float s = __fadd_rn(s0, part(v));
                     if (!last) {
                         const bool keep = valid && s <= thr;
-                        const unsigned ball = __ballot_sync(FULL, keep);
-                        if (keep) {
+                        const unsigned ball = __ballot_sync(FULL, keep) & EVEN;
+                        if (keep && hh == 0) {
                             const int o = nB + __popc(ball & lanemask_lt());
                             Bj[o] = j;
                             Bs[o] = s;
@@ -1182,10 +1169,10 @@ __global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, Screen
                         }
                         const float lb = lb_of(s, sl);
                         const bool surv = valid && lb <= ub;
-                        const unsigned ball = __ballot_sync(FULL, surv);
+                        const unsigned ball = __ballot_sync(FULL, surv) & EVEN;
                         const int add = __popc(ball);
                         if (nsv + add > SURV_CAP) flush();
-                        if (surv) {
+                        if (surv && hh == 0) {
                             const int o = nsv + __popc(ball & lanemask_lt());
                             sv_j[o] = j;
                             sv_lb[o] = lb;

@@ -329,7 +329,7 @@ __device__ __forceinline__ float ld_stream(const float *a, uint64_t pol)
 __device__ __forceinline__ uint4 ld_keep16(const uint4 *a, uint64_t pol)
 {
     uint4 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(a), "l"(pol));
     return v;

@@ -52,6 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(REPO, "include"),
            "-o", tmp, os.path.join(CSRC, "riann_b200.cu"),
            "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    if os.environ.get("RIANN_HANG_DEBUG"):
+        cmd.insert(1, "-DRIANN_HANG_DEBUG")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -482,6 +482,26 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
                  : "memory");
 }
 
+#ifdef RIANN_HANG_DEBUG
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    for (long long it = 0;; it++) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (1ll << 24)) {
+            printf("HANG block %d tid %d bar@%u parity %u\n", blockIdx.x, threadIdx.x, smem_addr(bar), parity);
+            __trap();
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
 {
     asm volatile(
@@ -492,6 +512,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
         "r"(parity)
         : "memory");
 }
+#endif
 
 __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
 {
@@ -523,16 +544,18 @@ __device__ __forceinline__ void filter_grab(const BulkParams &P, int &it, int &c
 
 // ---------------------------------------------------------------------------
 // Ring phase filter (search.py:133-134).  Work item (a, h): half h of anchor
-// a's rank row (entries j in [h n/2, (h+1) n/2), n bytes) plus the part-h list
-// ranges of the queries that drew a arrive in shared memory by TMA bulk copies
-// (one mbarrier); the staged 8-entry groups are spread evenly over all lanes,
-// each testing its alive entries: lo <= pos[a][j] < hi.  New alive bits go to
-// the other bit buffer, kept counts to kept[g].  The next item's descriptors
-// are fetched while the current copies fly; two CTAs per SM overlap one CTA's
-// copies with the other's filtering.
+// a's rank row (entries j in [h n/2, (h+1) n/2), n bytes) arrives in shared
+// memory by one TMA bulk copy; meanwhile every thread loads its 8-entry groups
+// of the queries' part-h lists and their alive bytes straight into registers
+// (groups spread evenly over the CTA: coalesced 16-byte loads), then tests its
+// alive entries: lo <= pos[a][j] < hi.  New alive bits go to the other bit
+// buffer, kept counts to kept[g].  The next item's descriptors are fetched
+// while the copy flies; two CTAs per SM overlap one CTA's copy with the
+// other's filtering.  (Staging the lists by per-query TMA copies instead costs
+// ~30 ns of TMA issue per copy: measured slower.)
 __host__ __device__ constexpr size_t filter_smem(int64_t n)
 {
-    return (size_t)n + LCAP * 2 + 2 * FCAP * 16 + (FCAP + 1) * 4;
+    return (size_t)n + 2 * FCAP * 16 + (FCAP + 1) * 4;
 }
 
 __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, int cur)
@@ -542,8 +565,7 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
     const int64_t n = P.n;
     const int jh = (int)(n >> 1);
     uint16_t *row = reinterpret_cast<uint16_t *>(smem_f);
-    uint16_t *stage = reinterpret_cast<uint16_t *>(smem_f + n);
-    int4 *descb = reinterpret_cast<int4 *>(smem_f + n + LCAP * 2);
+    int4 *descb = reinterpret_cast<int4 *>(smem_f + n);
     int *qg0 = reinterpret_cast<int *>(descb + 2 * FCAP);
     __shared__ uint64_t dbar[2], rbar;
     __shared__ int s_it[2], s_cnt[2], s_start[2], s_q1, s_ng;
@@ -611,19 +633,12 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                         s_q1 = q1;
                         s_ng = run;
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        mbar_expect_tx(&rbar, (unsigned)run * 16u + (first_sub ? (unsigned)n : 0u));
-                        if (first_sub)
+                        if (first_sub) {
+                            mbar_expect_tx(&rbar, (unsigned)n);
                             tma_bulk_g2s(row, P.pos + (int64_t)a * n + (int64_t)h * jh, (unsigned)n, &rbar);
-                    }
-                    __syncwarp();
-                    for (int i = q0 + lane; i < q1; i += 32) {
-                        const int4 d = desc[i];
-                        const int ng = h ? (d.w >> 17) : (d.z >> 17);
-                        if (ng > 0) {
-                            const int64_t src = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0);
-                            tma_bulk_g2s(stage + (int64_t)qg0[i - q0] * 8, P.pool + src, (unsigned)ng * 16u, &rbar);
                         }
                     }
+                    __syncwarp();
                 }
                 __syncthreads();
                 const int q1 = s_q1, NG = s_ng, mq = q1 - q0;
@@ -631,12 +646,14 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                 uint32_t al[NPRE];
                 int qi[NPRE];
                 int64_t eb[NPRE];
+                uint4 v[NPRE];
 #pragma unroll
                 for (int k = 0; k < NPRE; k++) {
                     const int G = k * FW2 * 32 + tid;
                     qi[k] = -1;
                     al[k] = 0;
                     eb[k] = 0;
+                    v[k] = make_uint4(0u, 0u, 0u, 0u);
                     if (G < NG) {
                         int x = 0, r = mq;  // last query with qg0 <= G
                         while (r - x > 1) {
@@ -648,6 +665,7 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                         qi[k] = x;
                         eb[k] = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0) + (int64_t)(G - qg0[x]) * 8;
                         al[k] = bcur[eb[k] >> 3];
+                        v[k] = *reinterpret_cast<const uint4 *>(P.pool + eb[k]);
                     }
                 }
                 // the next item and its descriptors, while the copies fly
@@ -659,8 +677,10 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                     s_start[db ^ 1] = nstart;
                     if (nit >= 0) fetch_desc(db ^ 1, nstart, min(ncnt, FCAP));
                 }
-                mbar_wait(&rbar, rpar);
-                rpar ^= 1;
+                if (first_sub) {
+                    mbar_wait(&rbar, rpar);
+                    rpar ^= 1;
+                }
                 const uint16_t *rowb = row - (int64_t)h * jh;  // indexed by j
 #pragma unroll
                 for (int k = 0; k < NPRE; k++) {
@@ -672,8 +692,7 @@ __global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, 
                         const int4 d = desc[q0 + qi[k]];
                         gq = d.x;
                         const int lo = d.z & 0x1ffff, hi = d.w & 0x1ffff;
-                        const uint4 v = *reinterpret_cast<const uint4 *>(stage + (int64_t)G * 8);
-                        const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
+                        const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
 #pragma unroll
                         for (int x = 0; x < 8; x++) {
                             if ((al[k] >> x) & 1u) {

@@ -365,18 +365,12 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
             return fail(RIANN_E_CUDA, "cublasSgemm failed");
         CK(cudaEventRecord(c->ev_proj, c->stream3));
     }
-    // P0
+    // P0a: d_prev, first-ring windows, list allocation (four queries per warp)
     {
-        const int wpb = 8;
-        const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
-        auto k = rb::bulk_p0_kernel<D>;
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        auto k = rb::bulk_p0a_kernel<D>;
         int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, wpb * 32, smem));
-        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::min(std::max(bps, 1), 8), (QN + wpb - 1) / wpb);
-        B.active_out = c->b_active[0].as<int32_t>();
-        B.n_active_out = ctr + 0;
-        k<<<(unsigned)std::max<int64_t>(blocks, 1), wpb * 32, smem, c->stream>>>(B);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, 0));
+        k<<<(unsigned)(c->sms * std::max(bps, 1)), 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
         c->launches += 1;
     }
@@ -399,6 +393,29 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         RET(r);
         c->launches += 1;
     }
+    // P0b: sorted fixed lists + alive bits (warp per query, bitmap in shared memory)
+    {
+        const int wpb = 8;
+        const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
+        auto k = rb::bulk_p0_kernel<D>;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, wpb * 32, smem));
+        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::min(std::max(bps, 1), 8), (QN + wpb - 1) / wpb);
+        B.active_out = c->b_active[0].as<int32_t>();
+        B.n_active_out = ctr + 0;
+        k<<<(unsigned)std::max<int64_t>(blocks, 1), wpb * 32, smem, c->stream>>>(B);
+        CK(cudaGetLastError());
+        c->launches += 1;
+    }
+    auto dk = rb::bulk_draw_kernel<D>;
+    int d_bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d_bps, dk, 256, 0));
+    const unsigned d_grid = (unsigned)(c->sms * std::max(d_bps, 1));
+    // first anchors (search.py:119-133): the draw kernel seeds each key's generator
+    dk<<<d_grid, 256, 0, c->stream>>>(B, 1);
+    CK(cudaGetLastError());
+    c->launches += 1;
     CK(cudaEventRecord(c->ev_heavy, c->stream2));
     B.heavy = c->b_heavy2.as<int32_t>();
     B.n_heavy = ctr + 6;
@@ -409,10 +426,6 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     int f_bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f_bps, fk, rb::FW2 * 32, fsmem));
     const unsigned f_grid = (unsigned)(c->sms * std::max(f_bps, 1));
-    auto dk = rb::bulk_draw_kernel<D>;
-    int d_bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d_bps, dk, 256, 0));
-    const unsigned d_grid = (unsigned)(c->sms * std::max(d_bps, 1));
     const unsigned small_grid = (unsigned)c->sms * 4;
     const int phases = Pq.max_rings - 1;
     for (int ph = 0; ph < phases; ph++) {

@@ -272,33 +272,22 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
     for (int i = lane; i < NW; i += 32) bm[i] = 0u;
     __syncwarp();
     for (int64_t g = gwarp; g < P.Q; g += nwarps) {
-        const float *q = P.units + g * D;
+        QState *sp = P.st + g;
+        // the state in one round: lane l (< 8) holds bytes 16 l .. 16 l + 15
+        uint4 sv = make_uint4(0u, 0u, 0u, 0u);
+        if (lane < 8) sv = reinterpret_cast<const uint4 *>(sp)[lane];
         const int p = P.prev[g];
-        if (p < 0 || p >= n) {
-            if (lane == 0) atomicExch(P.err, ERR_PREV_RANGE);
-            if (lane == 0) P.st[g].status = ST_HEAVY + 100;  // skipped everywhere
-            continue;
-        }
-        const double d = exact_dist_all<D>(P.refs, p, q, D, lane);
-        int64_t lo, hi;
-        window_coarse(P.sdist + (int64_t)p * n, P.coarse + (int64_t)p * P.ncoarse, P.ncoarse, n,
-                      __dsub_rn(d, __dmul_rn(P.alpha, d)), __dadd_rn(d, __dmul_rn(P.alpha, d)), lane, lo, hi);
-        const int cS = (int)(hi - lo);
-        const int alloc = (cS + 14 + 127) & ~127;  // >= lenA8 + lenB8; bits of a list 16-byte aligned
-        int64_t off = 0;
-        if (lane == 0 && cS <= LIGHT_MAX) {
-            off = (int64_t)atomicAdd(P.pool_top, (unsigned long long)alloc);
-            if (off + alloc > P.pool_cap) off = -1;
-        }
-        off = __shfl_sync(FULL, off, 0);
-        if (cS > LIGHT_MAX || off < 0) {
-            if (lane == 0) {
-                P.st[g].status = ST_HEAVY;
-                P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
-            }
-            continue;
-        }
-        // window of the u16 index row -> bitmap (16-byte vector loads on the aligned span)
+        auto word = [&](int wi) {
+            const uint32_t c = (wi & 3) == 0 ? sv.x : (wi & 3) == 1 ? sv.y : (wi & 3) == 2 ? sv.z : sv.w;
+            return __shfl_sync(FULL, c, wi >> 2);
+        };
+        if (word(15) != (uint32_t)ST_ACTIVE) continue;  // heavy (K2) or invalid prev
+        const int64_t lo = (int)word(26), hi = (int)word(27);
+        const int cS = (int)word(12);
+        const int64_t off = (int64_t)((uint64_t)word(2) | ((uint64_t)word(3) << 32));
+        const int alloc = (cS + 14 + 127) & ~127;
+        // window of the u16 index row -> bitmap; the aligned span's 16-byte loads
+        // are all issued before any marking (MB per lane per round)
         int cA = 0;  // entries of part A (j < n/2)
         {
             const uint16_t *row = P.sidx + (int64_t)p * n;
@@ -308,14 +297,29 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
             };
             const int64_t a0 = (lo + 7) & ~(int64_t)7, a1 = hi & ~(int64_t)7;
             if (a0 < a1) {
-                for (int64_t k = lo + lane; k < a0; k += 32) mark(__ldg(row + k));
-                for (int64_t v0 = a0 + (int64_t)lane * 8; v0 < a1; v0 += 256) {
-                    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + v0));
-                    const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v);
+                constexpr int MB = 8;
+                uint16_t hd = 0xffff, tl = 0xffff;
+                if (lo + lane < a0) hd = __ldg(row + lo + lane);
+                if (a1 + lane < hi) tl = __ldg(row + a1 + lane);
+                for (int64_t base = a0; base < a1; base += 256 * MB) {
+                    uint4 v[MB];
 #pragma unroll
-                    for (int x = 0; x < 8; x++) mark(e8[x]);
+                    for (int u = 0; u < MB; u++) {
+                        const int64_t v0 = base + (int64_t)(u * 32 + lane) * 8;
+                        v[u] = v0 < a1 ? __ldg(reinterpret_cast<const uint4 *>(row + v0)) : make_uint4(~0u, ~0u, ~0u, ~0u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < MB; u++) {
+                        const int64_t v0 = base + (int64_t)(u * 32 + lane) * 8;
+                        if (v0 < a1) {
+                            const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[u]);
+#pragma unroll
+                            for (int x = 0; x < 8; x++) mark(e8[x]);
+                        }
+                    }
                 }
-                for (int64_t k = a1 + lane; k < hi; k += 32) mark(__ldg(row + k));
+                if (lo + lane < a0) mark(hd);
+                if (a1 + lane < hi) mark(tl);
             } else {
                 for (int64_t k = lo + lane; k < hi; k += 32) mark(__ldg(row + k));
             }
@@ -385,59 +389,23 @@ __global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
                 b0[b] = v;
             }
         }
-        __threadfence_block();
-        __syncwarp();
-        // first anchor (search.py:119-131), drawn by lane 0
-        const bool loop = cS >= P.L && P.max_rings > 1 && cS - p_in > 0;
-        int an = -1, apos = -1;
-        Pcg64 rng;
-        if (lane == 0 && loop) {
-            seed_frame(rng, P, g);
-            int upos[1] = {below};
-            const int k = (int)pcg_integers(rng, (uint64_t)(cS - p_in));
-            const int r = avail_pos(k, upos, p_in);
-            apos = r + (r >= cA ? gap : 0);
-            an = (int)slot[apos];
-        }
-        an = __shfl_sync(FULL, an, 0);
-        int wlo = 0, whi = 0;
-        if (loop) anchor_window<D>(P, an, q, lane, wlo, whi);
+        // the first anchor is drawn by the draw kernel (rings 0 -> 1, S in bits0)
         if (lane == 0) {
-            QState s;
-            s.d_prev = d;
-            s.s_off = off;
-            s.cS = cS;
-            s.first = cS;
-            s.rings = 1;
-            s.tests = 0;
-            s.exact = 1;
-            s.lenA8 = lenA8;
-            s.lenB8 = lenB8;
-            s.pin_pos = p_in ? below + (p >= jh ? gap : 0) : -1;
-            s.sel = 0;
-            s.nu = 0;
-            s.rng_has = 0;
-            s.rng_buf = 0;
-            s.sh = s.sl = s.ih = s.il = 0;
-            s.anchor = 0;
-            s.lo = s.hi = 0;
-#pragma unroll
-            for (int k = 0; k < BULK_U; k++) s.up[k] = 0;
-            if (p_in) s.up[s.nu++] = (uint16_t)s.pin_pos;
-            if (loop) {
-                s.up[s.nu++] = (uint16_t)apos;
-                s.anchor = an;
-                s.lo = wlo;
-                s.hi = whi;
-                s.exact = 2;
-                rng_store(s, rng);
-                s.status = ST_ACTIVE;
-                P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
-            } else {
-                s.status = ST_DONE;
-            }
-            P.st[g] = s;
-            P.kept[g] = 0;
+            const int pin = p_in ? below + (p >= jh ? gap : 0) : -1;
+            sp->first = cS;
+            sp->rings = 0;
+            sp->tests = -cS;  // the draw adds |S|; the first ring is no membership test
+            sp->exact = 1;
+            sp->lenA8 = lenA8;
+            sp->lenB8 = lenB8;
+            sp->pin_pos = pin;
+            sp->sel = 0;
+            sp->nu = p_in ? 1 : 0;
+            sp->rng_has = 0;
+            sp->rng_buf = 0;
+            uint4 u4 = make_uint4(p_in ? (uint32_t)pin : 0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4 *>(sp->up) = u4;
+            P.kept[g] = cS;
         }
         __syncwarp();
     }
@@ -758,6 +726,142 @@ __device__ __forceinline__ int grp_sum(int v)
     return v;
 }
 
+// exact distance d of the query (qv) to reference a and the window [wlo, whi)
+// of row a for [d - alpha d, d + alpha d] (search.py:77-79), eight lanes:
+// level-1 index (32 entries) with the reference row, then 32 coarse entries,
+// then <= 63 row values.  act == false: no row reads past the first round.
+template <int D>
+__device__ __forceinline__ double dist_window8(const BulkParams &P, int a, const float (&qv)[D / 8], bool act, int gl,
+                                               int gb, int &wlo, int &whi)
+{
+    const int64_t n = P.n;
+    const int nb = P.ncoarse, cs1 = P.cs1;
+    float4 l1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) l1 = __ldg(reinterpret_cast<const float4 *>(P.coarse1 + (int64_t)a * 32) + gl);
+    const double da = dist8<D>(P.refs + (int64_t)a * D, qv, gl);
+    const double lv = __dsub_rn(da, __dmul_rn(P.alpha, da)), hv = __dadd_rn(da, __dmul_rn(P.alpha, da));
+    int b1lo, b1hi;
+    {
+        const float e[4] = {l1.x, l1.y, l1.z, l1.w};
+        int cl = 0, ch = 0;
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+            cl += (double)e[x] < lv ? 1 : 0;
+            ch += (double)e[x] <= hv ? 1 : 0;
+        }
+        b1lo = grp_sum(cl);
+        b1hi = grp_sum(ch);
+    }
+    // coarse round: lanes 0-3 of the group for lo, 4-7 for hi
+    const bool sh = gl >= 4;
+    const int sl = gl & 3;
+    const double thr = sh ? hv : lv;
+    int b;
+    {
+        const int b1 = sh ? b1hi : b1lo;
+        int cnt = 0;
+        const int cb = (b1 - 1) * cs1;
+        if (act && b1 > 0) {
+            const int cend = min(b1 * cs1, nb);
+            const float *cr = P.coarse + (int64_t)a * nb;
+#pragma unroll
+            for (int x = 0; x < 8; x++) {
+                const int ci = cb + 1 + sl * 8 + x;
+                if (ci < cend) {
+                    const double v = (double)__ldg(cr + ci);
+                    cnt += (sh ? v <= thr : v < thr) ? 1 : 0;
+                }
+            }
+        }
+        cnt += __shfl_xor_sync(FULL, cnt, 1);
+        cnt += __shfl_xor_sync(FULL, cnt, 2);
+        b = b1 > 0 ? cb + 1 + cnt : 0;
+    }
+    // fine round: <= 63 row values
+    int res;
+    {
+        const int64_t s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
+        const int64_t s1 = b < nb ? (int64_t)b * COARSE : n;
+        int cnt = 0;
+        if (act) {
+            const float *rr = P.sdist + (int64_t)a * n;
+#pragma unroll
+            for (int x = 0; x < 16; x++) {
+                const int64_t k = s0 + sl * 16 + x;
+                if (k < s1) {
+                    const double v = (double)__ldg(rr + k);
+                    cnt += (sh ? v <= thr : v < thr) ? 1 : 0;
+                }
+            }
+        }
+        cnt += __shfl_xor_sync(FULL, cnt, 1);
+        cnt += __shfl_xor_sync(FULL, cnt, 2);
+        res = (int)(s0 + cnt);
+    }
+    wlo = __shfl_sync(FULL, res, gb);
+    whi = __shfl_sync(FULL, res, gb | 4);
+    return da;
+}
+
+template <int D>
+__device__ __forceinline__ void load_qv8(const float *q, float (&qv)[D / 8], int gl)
+{
+    constexpr int HD = D > 128 ? D / 2 : D;
+#pragma unroll
+    for (int k = 0; k < HD / 8; k++) qv[k] = __ldg(q + gl + 8 * k);
+    if constexpr (D > 128) {
+#pragma unroll
+        for (int k = 0; k < HD / 8; k++) qv[HD / 8 + k] = __ldg(q + HD + gl + 8 * k);
+    }
+}
+
+// P0a (search.py:114-117): exact d_prev and the first-ring window on row prev,
+// the list allocation; four queries per warp, in index order.  Queries whose
+// first ring exceeds LIGHT_MAX (or the pool) go to K2.
+template <int D>
+__global__ void __launch_bounds__(256, 3) bulk_p0a_kernel(BulkParams P)
+{
+    const int lane = threadIdx.x & 31, gl = lane & 7, gb = lane & ~7;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t ib = gwarp * 4; ib < P.Q; ib += nwarps * 4) {
+        const int64_t gi = ib + (lane >> 3);
+        const int64_t g = gi < P.Q ? gi : 0;
+        const int p = P.prev[g];
+        const bool ok = gi < P.Q && p >= 0 && p < P.n;
+        if (gi < P.Q && !ok && gl == 0) {
+            atomicExch(P.err, ERR_PREV_RANGE);
+            P.st[g].status = ST_HEAVY + 100;  // skipped everywhere
+        }
+        if (!__any_sync(FULL, ok)) continue;
+        float qv[D / 8];
+        load_qv8<D>(P.units + g * D, qv, gl);
+        int lo, hi;
+        const double d = dist_window8<D>(P, ok ? p : 0, qv, ok, gl, gb, lo, hi);
+        if (ok && gl == 0) {
+            QState *sp = P.st + g;
+            const int cS = hi - lo;
+            const int alloc = (cS + 14 + 127) & ~127;  // >= lenA8 + lenB8; bits of a list 16-byte aligned
+            int64_t off = -1;
+            if (cS <= LIGHT_MAX) {
+                off = (int64_t)atomicAdd(P.pool_top, (unsigned long long)alloc);
+                if (off + alloc > P.pool_cap) off = -1;
+            }
+            sp->d_prev = d;
+            sp->lo = lo;
+            sp->hi = hi;
+            sp->cS = cS;
+            if (off < 0) {
+                sp->status = ST_HEAVY;
+                P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
+            } else {
+                sp->s_off = off;
+                sp->status = ST_ACTIVE;
+            }
+        }
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur)
 {
@@ -765,10 +869,7 @@ __global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur
     const int lane = threadIdx.x & 31, gl = lane & 7, gb = lane & ~7;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t n = P.n;
-    const int nb = P.ncoarse, cs1 = P.cs1;
     const uint8_t *bnxt = cur ? P.bits0 : P.bits1;
-    constexpr int HD = D > 128 ? D / 2 : D;
     // queries in index order (the state, unit rows, lists and bits then stream
     // sequentially); those filtered this phase have status ACTIVE
     for (int64_t ib = gwarp * 4; ib < P.Q; ib += nwarps * 4) {
@@ -782,15 +883,7 @@ __global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur
         if (!__any_sync(FULL, has)) continue;
         const int kept = has ? P.kept[g] : 0;
         float qv[D / 8];
-        {
-            const float *q = P.units + g * D;
-#pragma unroll
-            for (int k = 0; k < HD / 8; k++) qv[k] = __ldg(q + gl + 8 * k);
-            if constexpr (D > 128) {
-#pragma unroll
-                for (int k = 0; k < HD / 8; k++) qv[HD / 8 + k] = __ldg(q + HD + gl + 8 * k);
-            }
-        }
+        load_qv8<D>(P.units + g * D, qv, gl);
         auto word = [&](int wi) {  // 32-bit word wi of the state (compile-time wi)
             const uint32_t c = (wi & 3) == 0 ? sv.x : (wi & 3) == 1 ? sv.y : (wi & 3) == 2 ? sv.z : sv.w;
             return __shfl_sync(FULL, c, gb | (wi >> 2));
@@ -823,7 +916,10 @@ __global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur
         rng.has = (int)word(19);
         rng.buf = word(20);
         int kk = 0;
-        if (drew && gl == 0) kk = (int)pcg_integers(rng, (uint64_t)(kept - nua));
+        if (drew && gl == 0) {
+            if (rings == 1) seed_frame(rng, P, g);  // first draw (after P0): the key's generator (search.py:125-128)
+            kk = (int)pcg_integers(rng, (uint64_t)(kept - nua));
+        }
         kk = __shfl_sync(FULL, kk, gb);
         // avail[kk]: 32 bit words per round, 4 per lane
         int apos = -1;
@@ -879,70 +975,8 @@ __global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur
         int an = 0;
         if (drew && gl == 0) an = (int)P.pool[soff + apos];
         an = __shfl_sync(FULL, an, gb);
-        // exact d_a + level-1 row (one round)
-        float4 l1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (drew) l1 = __ldg(reinterpret_cast<const float4 *>(P.coarse1 + (int64_t)an * 32) + gl);
-        const double da = dist8<D>(P.refs + (int64_t)an * D, qv, gl);
-        const double lv = __dsub_rn(da, __dmul_rn(P.alpha, da)), hv = __dadd_rn(da, __dmul_rn(P.alpha, da));
-        int b1lo, b1hi;
-        {
-            const float e[4] = {l1.x, l1.y, l1.z, l1.w};
-            int cl = 0, ch = 0;
-#pragma unroll
-            for (int x = 0; x < 4; x++) {
-                cl += (double)e[x] < lv ? 1 : 0;
-                ch += (double)e[x] <= hv ? 1 : 0;
-            }
-            b1lo = grp_sum(cl);
-            b1hi = grp_sum(ch);
-        }
-        // coarse round: lanes 0-3 of the group for lo, 4-7 for hi
-        const bool sh = gl >= 4;
-        const int sl = gl & 3;
-        const double thr = sh ? hv : lv;
-        int b;
-        {
-            const int b1 = sh ? b1hi : b1lo;
-            int cnt = 0;
-            const int cb = (b1 - 1) * cs1;
-            if (drew && b1 > 0) {
-                const int cend = min(b1 * cs1, nb);
-                const float *cr = P.coarse + (int64_t)an * nb;
-#pragma unroll
-                for (int x = 0; x < 8; x++) {
-                    const int ci = cb + 1 + sl * 8 + x;
-                    if (ci < cend) {
-                        const double v = (double)__ldg(cr + ci);
-                        cnt += (sh ? v <= thr : v < thr) ? 1 : 0;
-                    }
-                }
-            }
-            cnt += __shfl_xor_sync(FULL, cnt, 1);
-            cnt += __shfl_xor_sync(FULL, cnt, 2);
-            b = b1 > 0 ? cb + 1 + cnt : 0;
-        }
-        // fine round: <= 63 row values
-        int res;
-        {
-            const int64_t s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
-            const int64_t s1 = b < nb ? (int64_t)b * COARSE : n;
-            int cnt = 0;
-            if (drew) {
-                const float *rr = P.sdist + (int64_t)an * n;
-#pragma unroll
-                for (int x = 0; x < 16; x++) {
-                    const int64_t k = s0 + sl * 16 + x;
-                    if (k < s1) {
-                        const double v = (double)__ldg(rr + k);
-                        cnt += (sh ? v <= thr : v < thr) ? 1 : 0;
-                    }
-                }
-            }
-            cnt += __shfl_xor_sync(FULL, cnt, 1);
-            cnt += __shfl_xor_sync(FULL, cnt, 2);
-            res = (int)(s0 + cnt);
-        }
-        const int wlo = __shfl_sync(FULL, res, gb), whi = __shfl_sync(FULL, res, gb | 4);
+        int wlo, whi;
+        dist_window8<D>(P, an, qv, drew, gl, gb, wlo, whi);
         if (has && gl == 0) {
             sp->tests += cS;
             sp->rings = rings;
@@ -959,10 +993,7 @@ __global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur
                 sp->hi = whi;
                 sp->up[nu] = (uint16_t)apos;
                 sp->nu = nu + 1;
-                sp->sh = rng.sh;
-                sp->sl = rng.sl;
-                sp->rng_has = rng.has;
-                sp->rng_buf = rng.buf;
+                rng_store(*sp, rng);
                 status = ST_ACTIVE;
                 P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
             } else if (want) {

@@ -17,7 +17,7 @@ import numpy as np
 from .errors import DimensionError, ModelCapacityError, RiannError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libriann_b200.so")
+LIB_PATH = os.environ.get("RIANN_LIB") or os.path.join(_PKG, "_lib", "libriann_b200.so")  # RIANN_LIB: development A/B builds
 
 OK, E_VALUE, E_DIMENSION, E_INDEX, E_CAPACITY, E_UNSUPPORTED, E_CUDA, E_STATE = range(8)
 F_TEMPORAL, F_DEVICE_PTRS, F_ASYNC, F_KEEP_UNITS = 1, 2, 4, 8

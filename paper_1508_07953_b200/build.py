@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
-LIB = os.path.join(LIB_DIR, "libriann_b200.so")
+LIB = os.environ.get("RIANN_LIB") or os.path.join(LIB_DIR, "libriann_b200.so")  # RIANN_LIB: development A/B builds
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -46,7 +46,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     tmp = LIB + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(REPO, "include"),
@@ -54,6 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     if os.environ.get("RIANN_HANG_DEBUG"):
         cmd.insert(1, "-DRIANN_HANG_DEBUG")
+    for d in os.environ.get("RIANN_NVCC_DEFS", "").split():  # development A/B builds
+        cmd.insert(1, d)
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

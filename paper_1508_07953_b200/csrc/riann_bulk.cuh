@@ -30,13 +30,27 @@
 
 #include "riann_kernels.cuh"
 
+// occupancy knobs (development A/B builds override them with -D)
+#ifndef RIANN_FINAL_FB
+#define RIANN_FINAL_FB 512
+#endif
+#ifndef RIANN_FINAL_MINB
+#define RIANN_FINAL_MINB 3
+#endif
+#ifndef RIANN_DRAW_MINB
+#define RIANN_DRAW_MINB 4
+#endif
+
 namespace rb {
 
 constexpr int LIGHT_MAX = 16384;  // largest first ring handled by the bulk path (u16 entries)
 constexpr int BULK_U = 8;        // used anchors tracked per query (prev + 7 draws at max_rings = 8)
 constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 constexpr int FCAP = 256;        // query descriptors per filter stage
-constexpr int FW2 = 16;          // warps per filter CTA
+#ifndef RIANN_FILTER_WARPS
+#define RIANN_FILTER_WARPS 16
+#endif
+constexpr int FW2 = RIANN_FILTER_WARPS;  // warps per filter CTA
 constexpr int LCAP = 16384;      // list entries staged per filter sub-chunk
 constexpr int FSEG = 256;        // list entries per final-scan fill round (8 per lane)
 
@@ -526,7 +540,7 @@ __host__ __device__ constexpr size_t filter_smem(int64_t n)
     return (size_t)n + 2 * FCAP * 16 + (FCAP + 1) * 4;
 }
 
-__global__ void __launch_bounds__(FW2 * 32, 2) bulk_filter_kernel(BulkParams P, int cur)
+__global__ void __launch_bounds__(FW2 * 32, 32 / FW2 < 3 ? 32 / FW2 : 3) bulk_filter_kernel(BulkParams P, int cur)
 {
     extern __shared__ __align__(128) unsigned char smem_f[];
     constexpr int NPRE = LCAP / 8 / (FW2 * 32);  // staged groups per thread
@@ -863,7 +877,7 @@ __global__ void __launch_bounds__(256, 3) bulk_p0a_kernel(BulkParams P)
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 3) bulk_draw_kernel(BulkParams P, int cur)
+__global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkParams P, int cur)
 {
     static_assert(D % 8 == 0 && D <= 256, "draw kernel dims");
     const int lane = threadIdx.x & 31, gl = lane & 7, gb = lane & ~7;
@@ -1027,10 +1041,10 @@ struct ScreenParams {
     float one_plus_eta, one_minus_eta;
 };
 
-constexpr int FB = 512;  // candidates per screening block
+constexpr int FB = RIANN_FINAL_FB;  // candidates per screening block
 
 template <int D>
-__global__ void __launch_bounds__(256, 3) bulk_final_kernel(BulkParams P, ScreenParams SP)
+__global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkParams P, ScreenParams SP)
 {
     constexpr int GX = Lay<D>::G;
     constexpr int NGX = WARP / GX;

@@ -438,3 +438,28 @@ def test_model_switch_smaller_n(R, oracle_mod):
         assert np.array_equal(fld.indices, idx), t
         assert np.array_equal(_bits(fld.distances), _bits(dist)), t
         prev = idx
+
+
+@pytest.mark.parametrize("L,alpha,max_rings", [(4, 0.3, 12), (1, 0.25, 2), (50, 0.1, 8)])
+def test_frame_path_search_params(R, oracle_mod, L, alpha, max_rings):
+    """Non-default SearchParams through the bulk path: long ring caps (more
+    used anchors than the draw kernel tracks: those queries are finished by K2
+    from scratch), a single ring phase, a large L.  Bit-identical to the oracle."""
+    from paper_1508_07953_b200 import workloads as W
+
+    cfg = W.CONFIGS[0]
+    frames = W.clip(cfg, 3)
+    refs = W.reference_set(cfg)
+    model = R.ReferenceModel.from_refs(refs, cfg.patch)
+    sd, si = model.table_rows(0, model.n)
+    om = oracle_mod.OracleModel(refs, sd, si)
+    gw, gh = cfg.grid
+    prev = oracle_mod.init_field_indices(gw, gh, model.n, 0)
+    params = R.SearchParams(L=L, alpha=alpha, max_rings=max_rings)
+    for t, (_, fld, st) in enumerate(R.stream_fields(model, frames, params)):
+        idx, dist, ost, _ = oracle_mod.process_frame(om, frames[t], prev, cfg.patch, t + 1, L=L, alpha=alpha,
+                                                     max_rings=max_rings)
+        assert np.array_equal(fld.indices, idx), t
+        assert np.array_equal(_bits(fld.distances), _bits(dist)), t
+        assert st.total_rings == ost["total_rings"] and st.total_distance_evals == ost["total_distance_evals"]
+        prev = idx

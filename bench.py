@@ -435,8 +435,8 @@ def run_ours(a):
                              "no flush", "table_build_s": t_tables, "data_gen_s": t_data},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "query path: bulk_p0 + 7 bulk_ring phases + bulk_final (+ query_kernel "
-                                   "fallback), one CUDA-event window per frame",
+                         "kernel": "query path: bulk_p0a + bulk_p0 + 8 draw + 7 (group + filter) ring phases + "
+                                   "bulk_final (+ query_kernel fallback), one CUDA-event window per frame",
                          "kernel_ms_per_frame": k2_ms / K,
                          "units_kernel_ms_per_frame": allmax(ms3[0]) / K,
                          "note": "achieved counts SURVEY 8d algorithmic bytes (4*D per distance evaluation) "

@@ -427,6 +427,10 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f_bps, fk, rb::FW2 * 32, fsmem));
     const unsigned f_grid = (unsigned)(c->sms * std::max(f_bps, 1));
     const unsigned small_grid = (unsigned)c->sms * 4;
+    auto wk = rb::bulk_window_kernel<D>;
+    int w_bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w_bps, wk, 256, 0));
+    const unsigned w_grid = (unsigned)(c->sms * std::max(w_bps, 1));
     const int phases = Pq.max_rings - 1;
     for (int ph = 0; ph < phases; ph++) {
         const int in = ph & 1, out = in ^ 1;
@@ -449,11 +453,13 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
+        wk<<<w_grid, 256, 0, c->stream>>>(B);
+        CK(cudaGetLastError());
         fk<<<f_grid, rb::FW2 * 32, fsmem, c->stream>>>(B, ph & 1);
         CK(cudaGetLastError());
         dk<<<d_grid, 256, 0, c->stream>>>(B, ph & 1);
         CK(cudaGetLastError());
-        c->launches += 4;
+        c->launches += 5;
     }
     // final scan of the light queries (PCA-basis screening)
     {

@@ -37,8 +37,11 @@
 #ifndef RIANN_FINAL_MINB
 #define RIANN_FINAL_MINB 3
 #endif
+#ifndef RIANN_WIN_MINB
+#define RIANN_WIN_MINB 4
+#endif
 #ifndef RIANN_DRAW_MINB
-#define RIANN_DRAW_MINB 4
+#define RIANN_DRAW_MINB 5
 #endif
 
 namespace rb {
@@ -896,8 +899,6 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
         if (!has) sv = make_uint4(0u, 0u, 0u, 0u);
         if (!__any_sync(FULL, has)) continue;
         const int kept = has ? P.kept[g] : 0;
-        float qv[D / 8];
-        load_qv8<D>(P.units + g * D, qv, gl);
         auto word = [&](int wi) {  // 32-bit word wi of the state (compile-time wi)
             const uint32_t c = (wi & 3) == 0 ? sv.x : (wi & 3) == 1 ? sv.y : (wi & 3) == 2 ? sv.z : sv.w;
             return __shfl_sync(FULL, c, gb | (wi >> 2));
@@ -989,8 +990,6 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
         int an = 0;
         if (drew && gl == 0) an = (int)P.pool[soff + apos];
         an = __shfl_sync(FULL, an, gb);
-        int wlo, whi;
-        dist_window8<D>(P, an, qv, drew, gl, gb, wlo, whi);
         if (has && gl == 0) {
             sp->tests += cS;
             sp->rings = rings;
@@ -1003,8 +1002,6 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
             if (drew) {
                 sp->exact += 1;
                 sp->anchor = an;
-                sp->lo = wlo;
-                sp->hi = whi;
                 sp->up[nu] = (uint16_t)apos;
                 sp->nu = nu + 1;
                 rng_store(*sp, rng);
@@ -1015,6 +1012,39 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
                 P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;
             }
             sp->status = status;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Ring phase window (search.py:131-133), after grouping: for the active
+// queries in anchor order (four per warp, eight lanes each) the exact d_a and
+// the window [lo, hi) on the anchor's sorted row, written into the queries'
+// descriptors.  Consecutive queries share their anchor, so its reference row,
+// level-1 and coarse entries are served by L1.
+template <int D>
+__global__ void __launch_bounds__(256, RIANN_WIN_MINB) bulk_window_kernel(BulkParams P)
+{
+    const int lane = threadIdx.x & 31, gl = lane & 7, gb = lane & ~7;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int m = *P.n_active_in;
+    for (int64_t ib = gwarp * 4; ib < m; ib += nwarps * 4) {
+        const int64_t i = ib + (lane >> 3);
+        const bool has = i < m;
+        int4 d = has ? P.gdesc[i] : make_int4(0, 0, 0, 0);
+        const int64_t g = has ? d.x : 0;
+        int a = 0;
+        if (has && gl == 0) a = P.st[g].anchor;
+        a = __shfl_sync(FULL, a, gb);
+        float qv[D / 8];
+        load_qv8<D>(P.units + g * D, qv, gl);
+        int lo, hi;
+        dist_window8<D>(P, a, qv, has, gl, gb, lo, hi);
+        if (has && gl == 0) {
+            d.z = (d.z & ~0x1ffff) | lo;
+            d.w = (d.w & ~0x1ffff) | hi;
+            P.gdesc[i] = d;
         }
     }
 }

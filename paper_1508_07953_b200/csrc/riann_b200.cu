@@ -395,7 +395,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     }
     // P0b: sorted fixed lists + alive bits (warp per query, bitmap in shared memory)
     {
-        const int wpb = 8;
+        const int wpb = RIANN_P0_WPB;
         const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
         auto k = rb::bulk_p0_kernel<D>;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -37,6 +37,18 @@
 #ifndef RIANN_FINAL_MINB
 #define RIANN_FINAL_MINB 3
 #endif
+#ifndef RIANN_P0_WPB
+#define RIANN_P0_WPB 8
+#endif
+#ifndef RIANN_P0A_MINB
+#define RIANN_P0A_MINB 3
+#endif
+#ifndef RIANN_FILTER_MINB
+#define RIANN_FILTER_MINB 2
+#endif
+#ifndef RIANN_FILTER_LCAP
+#define RIANN_FILTER_LCAP 16384
+#endif
 #ifndef RIANN_WIN_MINB
 #define RIANN_WIN_MINB 4
 #endif
@@ -54,7 +66,8 @@ constexpr int FCAP = 256;        // query descriptors per filter stage
 #define RIANN_FILTER_WARPS 16
 #endif
 constexpr int FW2 = RIANN_FILTER_WARPS;  // warps per filter CTA
-constexpr int LCAP = 16384;      // list entries staged per filter sub-chunk
+constexpr int LCAP = RIANN_FILTER_LCAP;  // list entries per filter sub-chunk
+static_assert(LCAP >= LIGHT_MAX, "a query's list part (<= LIGHT_MAX entries) must fit one filter sub-chunk");
 constexpr int FSEG = 256;        // list entries per final-scan fill round (8 per lane)
 
 enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
@@ -274,7 +287,7 @@ __device__ __forceinline__ int bit_at(const uint8_t *bits, int64_t e) { return (
 __host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 4095) / 4096) * 128); }
 
 template <int D>
-__global__ void __launch_bounds__(256, 3) bulk_p0_kernel(BulkParams P)
+__global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_kernel(BulkParams P)
 {
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int lane = threadIdx.x & 31;
@@ -543,7 +556,7 @@ __host__ __device__ constexpr size_t filter_smem(int64_t n)
     return (size_t)n + 2 * FCAP * 16 + (FCAP + 1) * 4;
 }
 
-__global__ void __launch_bounds__(FW2 * 32, 32 / FW2 < 3 ? 32 / FW2 : 3) bulk_filter_kernel(BulkParams P, int cur)
+__global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kernel(BulkParams P, int cur)
 {
     extern __shared__ __align__(128) unsigned char smem_f[];
     constexpr int NPRE = LCAP / 8 / (FW2 * 32);  // staged groups per thread
@@ -836,7 +849,7 @@ __device__ __forceinline__ void load_qv8(const float *q, float (&qv)[D / 8], int
 // the list allocation; four queries per warp, in index order.  Queries whose
 // first ring exceeds LIGHT_MAX (or the pool) go to K2.
 template <int D>
-__global__ void __launch_bounds__(256, 3) bulk_p0a_kernel(BulkParams P)
+__global__ void __launch_bounds__(256, RIANN_P0A_MINB) bulk_p0a_kernel(BulkParams P)
 {
     const int lane = threadIdx.x & 31, gl = lane & 7, gb = lane & ~7;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;

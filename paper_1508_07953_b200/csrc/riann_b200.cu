@@ -473,7 +473,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         SP.one_plus_eta = 1.0f + c->pca_eta * 1.001f;
         SP.one_minus_eta = 1.0f - c->pca_eta * 1.001f;
         auto k = rb::bulk_final_kernel<D>;
-        const size_t smem = 8 * (2 * rb::FB * 8 + 128 * 8);
+        const size_t smem = 8 * rb::final_warp_bytes();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int bps = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, smem));

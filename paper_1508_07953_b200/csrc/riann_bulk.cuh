@@ -1085,6 +1085,12 @@ struct ScreenParams {
 };
 
 constexpr int FB = RIANN_FINAL_FB;  // candidates per screening block
+#ifndef RIANN_FINAL_U16
+#define RIANN_FINAL_U16 1
+#endif
+using FIdx = std::conditional_t<RIANN_FINAL_U16 != 0, uint16_t, uint32_t>;  // candidate index in the final scan (n <= 65,536)
+constexpr int FSURV = 128;
+__host__ __device__ constexpr size_t final_warp_bytes() { return (size_t)FB * (8 + 2 * sizeof(FIdx)) + FSURV * 8; }
 
 template <int D>
 __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkParams P, ScreenParams SP)
@@ -1092,19 +1098,20 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
     constexpr int GX = Lay<D>::G;
     constexpr int NGX = WARP / GX;
     constexpr int NCH = D / 16;
-    constexpr int SURV_CAP = 128;
+    constexpr int SURV_CAP = FSURV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     // per warp: two (index, partial) lists of FB entries + survivor slots
-    unsigned char *ws = smem_raw + (size_t)wib * (2 * FB * 8 + SURV_CAP * 8);
-    uint32_t *Aj = reinterpret_cast<uint32_t *>(ws);
-    float *As = reinterpret_cast<float *>(ws + FB * 4);
-    uint32_t *Bj = reinterpret_cast<uint32_t *>(ws + FB * 8);
-    float *Bs = reinterpret_cast<float *>(ws + FB * 12);
-    uint32_t *sv_j = reinterpret_cast<uint32_t *>(ws + FB * 16);
-    float *sv_lb = reinterpret_cast<float *>(ws + FB * 16 + SURV_CAP * 4);
+    // per warp: partial sums As/Bs (f32), candidate lists Aj/Bj (FIdx), survivors
+    unsigned char *ws = smem_raw + (size_t)wib * final_warp_bytes();
+    float *As = reinterpret_cast<float *>(ws);
+    float *Bs = reinterpret_cast<float *>(ws + FB * 4);
+    FIdx *Aj = reinterpret_cast<FIdx *>(ws + FB * 8);
+    FIdx *Bj = reinterpret_cast<FIdx *>(ws + FB * 8 + FB * sizeof(FIdx));
+    uint32_t *sv_j = reinterpret_cast<uint32_t *>(ws + FB * (8 + 2 * sizeof(FIdx)));
+    float *sv_lb = reinterpret_cast<float *>(ws + FB * (8 + 2 * sizeof(FIdx)) + SURV_CAP * 4);
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const uint64_t pol_keep = pol_evict_last();
     unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
@@ -1162,7 +1169,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
         float thr = thr_of(ub);
         for (int lp = 0; lp < Wl;) {
             // S = the alive list entries: up to FB of them into Bj's space
-            uint32_t *Cj = Bj;
+            FIdx *Cj = Bj;
             int bn = 0;
             while (lp < Wl && bn <= FB - FSEG) {
                 const int e0 = lp + lane * 8;
@@ -1290,7 +1297,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                 __syncwarp();
                 if (!last) {
                     // swap lists
-                    uint32_t *tj = Aj;
+                    FIdx *tj = Aj;
                     float *ts = As;
                     Aj = Bj;
                     As = Bs;

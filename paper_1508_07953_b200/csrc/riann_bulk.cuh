@@ -58,7 +58,7 @@
 
 namespace rb {
 
-constexpr int LIGHT_MAX = 16384;  // largest first ring handled by the bulk path (u16 entries)
+constexpr int LIGHT_MAX = 32752;  // largest first ring handled by the bulk path (part lengths / 8 fit 12 descriptor bits)
 constexpr int BULK_U = 8;        // used anchors tracked per query (prev + 7 draws at max_rings = 8)
 constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 constexpr int FCAP = 256;        // query descriptors per filter stage
@@ -67,7 +67,6 @@ constexpr int FCAP = 256;        // query descriptors per filter stage
 #endif
 constexpr int FW2 = RIANN_FILTER_WARPS;  // warps per filter CTA
 constexpr int LCAP = RIANN_FILTER_LCAP;  // list entries per filter sub-chunk
-static_assert(LCAP >= LIGHT_MAX, "a query's list part (<= LIGHT_MAX entries) must fit one filter sub-chunk");
 constexpr int FSEG = 256;        // list entries per final-scan fill round (8 per lane)
 
 enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
@@ -606,60 +605,57 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                 mbar_wait(&dbar[1], dpar1);
                 dpar1 ^= 1;
             }
-            for (int q0 = 0; q0 < m;) {
-                // warp 0: sub-chunk [q0, q1) whose part-h lists fit the staging
-                // buffer, their staged group offsets, and the copies
-                if (w == 0) {
-                    int run = 0, q1 = q0;
-                    for (int b = q0; b < m; b += 32) {
-                        const int i = b + lane;
-                        int ng = 0;
-                        if (i < m) {
-                            const int4 d = desc[i];
-                            ng = h ? (d.w >> 17) : (d.z >> 17);
-                        }
-                        const int inc = warp_incl_scan(ng, lane);
-                        const bool fits = i < m && (run + inc) * 8 <= LCAP;
-                        const int nf = __popc(__ballot_sync(FULL, fits));
-                        if (fits) qg0[i - q0] = run + inc - ng;
-                        if (nf > 0) run += __shfl_sync(FULL, inc, nf - 1);
-                        q1 = b + nf;
-                        if (nf < 32) break;
+            // warp 0: group offsets of the chunk's queries (part h) and the row copy
+            if (w == 0) {
+                int run = 0;
+                for (int b = 0; b < m; b += 32) {
+                    const int i = b + lane;
+                    int ng = 0;
+                    if (i < m) {
+                        const int4 d = desc[i];
+                        ng = h ? (d.w >> 17) : (d.z >> 17);
                     }
-                    if (lane == 0) {
-                        qg0[q1 - q0] = run;
-                        s_q1 = q1;
-                        s_ng = run;
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        if (first_sub) {
-                            mbar_expect_tx(&rbar, (unsigned)n);
-                            tma_bulk_g2s(row, P.pos + (int64_t)a * n + (int64_t)h * jh, (unsigned)n, &rbar);
-                        }
-                    }
-                    __syncwarp();
+                    const int inc = warp_incl_scan(ng, lane);
+                    if (i < m) qg0[i] = run + inc - ng;
+                    run += __shfl_sync(FULL, inc, 31);
                 }
-                __syncthreads();
-                const int q1 = s_q1, NG = s_ng, mq = q1 - q0;
-                // alive bytes of my groups (independent of the copies)
+                if (lane == 0) {
+                    qg0[m] = run;
+                    s_ng = run;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (first_sub) {
+                        mbar_expect_tx(&rbar, (unsigned)n);
+                        tma_bulk_g2s(row, P.pos + (int64_t)a * n + (int64_t)h * jh, (unsigned)n, &rbar);
+                    }
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            const int NGt = s_ng;
+            // sub-chunks of GC groups; a query's groups may span sub-chunks
+            constexpr int GC = NPRE * FW2 * 32;
+            for (int G0 = 0; G0 < NGt || (first_sub && G0 == 0); G0 += GC) {
+                const int NG = min(GC, NGt - G0);
+                // list groups and alive bytes of my groups (independent of the row copy)
                 uint32_t al[NPRE];
                 int qi[NPRE];
                 int64_t eb[NPRE];
                 uint4 v[NPRE];
 #pragma unroll
                 for (int k = 0; k < NPRE; k++) {
-                    const int G = k * FW2 * 32 + tid;
+                    const int G = G0 + k * FW2 * 32 + tid;
                     qi[k] = -1;
                     al[k] = 0;
                     eb[k] = 0;
                     v[k] = make_uint4(0u, 0u, 0u, 0u);
-                    if (G < NG) {
-                        int x = 0, r = mq;  // last query with qg0 <= G
+                    if (G < G0 + NG) {
+                        int x = 0, r = m;  // last query with qg0 <= G
                         while (r - x > 1) {
                             const int mid = (x + r) >> 1;
                             if (qg0[mid] <= G) x = mid;
                             else r = mid;
                         }
-                        const int4 d = desc[q0 + x];
+                        const int4 d = desc[x];
                         qi[k] = x;
                         eb[k] = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0) + (int64_t)(G - qg0[x]) * 8;
                         al[k] = bcur[eb[k] >> 3];
@@ -683,11 +679,10 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
 #pragma unroll
                 for (int k = 0; k < NPRE; k++) {
                     if (k * FW2 * 32 >= NG) break;  // block-uniform
-                    const int G = k * FW2 * 32 + tid;
                     uint32_t keep = 0;
                     int gq = -1;
                     if (qi[k] >= 0) {
-                        const int4 d = desc[q0 + qi[k]];
+                        const int4 d = desc[qi[k]];
                         gq = d.x;
                         const int lo = d.z & 0x1ffff, hi = d.w & 0x1ffff;
                         const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
@@ -710,7 +705,6 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                     }
                 }
                 first_sub = false;
-                q0 = q1;
                 __syncthreads();
             }
         }

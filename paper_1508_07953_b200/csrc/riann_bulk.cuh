@@ -58,7 +58,7 @@
 
 namespace rb {
 
-constexpr int LIGHT_MAX = 32752;  // largest first ring handled by the bulk path (part lengths / 8 fit 12 descriptor bits)
+constexpr int LIGHT_MAX = 32752;  // largest first ring handled by the bulk path (u16 list positions)
 constexpr int BULK_U = 8;        // used anchors tracked per query (prev + 7 draws at max_rings = 8)
 constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 constexpr int FCAP = 256;        // query descriptors per filter stage

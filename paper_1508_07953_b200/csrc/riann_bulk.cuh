@@ -520,24 +520,6 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigne
         : "memory");
 }
 
-// next non-empty (anchor, half) work item of the filter phase
-__device__ __forceinline__ void filter_grab(const BulkParams &P, int &it, int &cnt, int &start)
-{
-    for (;;) {
-        const int i = atomicAdd(P.item_next, 1);
-        if (i >= 2 * P.n) {
-            it = -1;
-            return;
-        }
-        const int c = P.counts[i >> 1];
-        if (c > 0) {
-            it = i;
-            cnt = c;
-            start = P.starts[i >> 1];
-            return;
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Ring phase filter (search.py:133-134).  Work item (a, h): half h of anchor
@@ -574,16 +556,56 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
         mbar_expect_tx(&dbar[b], (unsigned)m * 16u);
         tma_bulk_g2s(descb + b * FCAP, P.gdesc + start, (unsigned)m * 16u, &dbar[b]);
     };
+    // work items: batches of FGRAB consecutive (anchor, half) items taken with
+    // one atomic; warp 1 reads a batch's counts / starts in one load round into
+    // a lane window, so only one item in FGRAB waits on memory
+    constexpr int FGRAB = 16;
+    const int nitems = (int)(2 * n);
+    int win_it = -1, win_cnt = 0, win_start = 0;  // per lane of warp 1
+    unsigned win_mask = 0;
+    bool drained = false;
+    auto next_item = [&](int &it, int &cnt, int &start) {  // all lanes of warp 1
+        it = -1;
+        cnt = start = 0;
+        while (it < 0) {
+            if (win_mask == 0) {
+                if (drained) return;
+                int base = 0;
+                if (lane == 0) base = atomicAdd(P.item_next, FGRAB);
+                base = __shfl_sync(FULL, base, 0);
+                if (base >= nitems) {
+                    drained = true;
+                    return;
+                }
+                const int i = base + lane;
+                win_it = (lane < FGRAB && i < nitems) ? i : -1;
+                win_cnt = win_it >= 0 ? P.counts[i >> 1] : 0;
+                win_start = win_cnt > 0 ? P.starts[i >> 1] : 0;
+                win_mask = __ballot_sync(FULL, win_cnt > 0);
+                continue;
+            }
+            const int l = __ffs(win_mask) - 1;
+            win_mask &= win_mask - 1;
+            it = __shfl_sync(FULL, win_it, l);
+            cnt = __shfl_sync(FULL, win_cnt, l);
+            start = __shfl_sync(FULL, win_start, l);
+        }
+    };
     if (tid == 0) {
         mbar_init(&dbar[0], 1);
         mbar_init(&dbar[1], 1);
         mbar_init(&rbar, 1);
-        int it, cnt = 0, start = 0;
-        filter_grab(P, it, cnt, start);
-        s_it[0] = it;
-        s_cnt[0] = cnt;
-        s_start[0] = start;
-        if (it >= 0) fetch_desc(0, start, min(cnt, FCAP));
+    }
+    __syncthreads();
+    if (w == 1) {
+        int it, cnt, start;
+        next_item(it, cnt, start);
+        if (lane == 0) {
+            s_it[0] = it;
+            s_cnt[0] = cnt;
+            s_start[0] = start;
+            if (it >= 0) fetch_desc(0, start, min(cnt, FCAP));
+        }
     }
     __syncthreads();
     unsigned dpar0 = 0, dpar1 = 0, rpar = 0;
@@ -663,13 +685,15 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                     }
                 }
                 // the next item and its descriptors, while the copies fly
-                if (first_sub && c0 == 0 && w == 1 && lane == 0) {
-                    int nit, ncnt = 0, nstart = 0;
-                    filter_grab(P, nit, ncnt, nstart);
-                    s_it[db ^ 1] = nit;
-                    s_cnt[db ^ 1] = ncnt;
-                    s_start[db ^ 1] = nstart;
-                    if (nit >= 0) fetch_desc(db ^ 1, nstart, min(ncnt, FCAP));
+                if (first_sub && c0 == 0 && w == 1) {
+                    int nit, ncnt, nstart;
+                    next_item(nit, ncnt, nstart);
+                    if (lane == 0) {
+                        s_it[db ^ 1] = nit;
+                        s_cnt[db ^ 1] = ncnt;
+                        s_start[db ^ 1] = nstart;
+                        if (nit >= 0) fetch_desc(db ^ 1, nstart, min(ncnt, FCAP));
+                    }
                 }
                 if (first_sub) {
                     mbar_wait(&rbar, rpar);

@@ -463,3 +463,24 @@ def test_frame_path_search_params(R, oracle_mod, L, alpha, max_rings):
         assert np.array_equal(_bits(fld.distances), _bits(dist)), t
         assert st.total_rings == ost["total_rings"] and st.total_distance_evals == ost["total_distance_evals"]
         prev = idx
+
+
+def test_frame_path_k2_only_model(R, oracle_mod):
+    """n % 16 != 0: the bulk path declines the model and every query runs K2;
+    still bit-identical to the oracle."""
+    from paper_1508_07953_b200 import workloads as W
+
+    cfg = W.CONFIGS[0]
+    frames = W.clip(cfg, 3)
+    refs = W.reference_set(cfg)[:1000]
+    model = R.ReferenceModel.from_refs(refs, cfg.patch)
+    sd, si = model.table_rows(0, model.n)
+    om = oracle_mod.OracleModel(refs, sd, si)
+    gw, gh = cfg.grid
+    prev = oracle_mod.init_field_indices(gw, gh, model.n, 0)
+    for t, (_, fld, st) in enumerate(R.stream_fields(model, frames)):
+        idx, dist, ost, _ = oracle_mod.process_frame(om, frames[t], prev, cfg.patch, t + 1)
+        assert np.array_equal(fld.indices, idx), t
+        assert np.array_equal(_bits(fld.distances), _bits(dist)), t
+        assert st.total_rings == ost["total_rings"] and st.total_distance_evals == ost["total_distance_evals"]
+        prev = idx

@@ -173,7 +173,7 @@ struct riann_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;  // heavy-query fallback, concurrent with the ring phases
     cudaStream_t stream3 = nullptr;  // final-scan projection, concurrent with P0 / ring phases
-    cudaEvent_t ev_p0 = nullptr, ev_heavy = nullptr, ev_units = nullptr, ev_proj = nullptr;
+    cudaEvent_t ev_p0 = nullptr, ev_heavy = nullptr, ev_units = nullptr, ev_proj = nullptr, ev_tc = nullptr;
     int sms = 0;
     int smem_optin = 0;
     // model
@@ -848,6 +848,7 @@ int riann_ctx_create(int device, riann_ctx **out)
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_units, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_proj, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_tc, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         delete c;
         return fail(RIANN_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
@@ -888,6 +889,7 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaEventDestroy(c->ev_heavy);
     cudaEventDestroy(c->ev_units);
     cudaEventDestroy(c->ev_proj);
+    cudaEventDestroy(c->ev_tc);
     cudaStreamDestroy(c->stream2);
     cudaStreamDestroy(c->stream3);
     cudaStreamDestroy(c->stream);
@@ -1197,12 +1199,12 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
     P.stats = c->stats.as<unsigned long long>();
     P.err = c->err.as<int>();
     if (c->timing) CK(cudaEventRecord(evs[1], c->stream));
-    if (Q > 0) {
-        RET(launch_query(c, P));
-        c->launches += 1;
-    }
-    if (c->timing) CK(cudaEventRecord(evs[2], c->stream));
-    if (temporal && Q > 0) {
+    // temporal-change reduction: needs only K1's per-position values, so it
+    // runs on the third stream alongside the query path
+    const bool tree = temporal && Q > 0;
+    if (tree) {
+        CK(cudaEventRecord(c->ev_tc, c->stream));
+        CK(cudaStreamWaitEvent(c->stream3, c->ev_tc, 0));
         RET(c->tree.build(Q));
         rb::PwTreeParams T;
         T.vals = c->tc.as<double>();
@@ -1217,10 +1219,17 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         T.right = c->tree.right.as<int32_t>();
         T.node_val = c->tree.node_val.as<double>();
         T.out = c->tc_sum.as<double>();
-        rb::pw_tree_kernel<<<1, 1024, 0, c->stream>>>(T);
+        rb::pw_tree_kernel<<<1, 1024, 0, c->stream3>>>(T);
         CK(cudaGetLastError());
+        CK(cudaEventRecord(c->ev_tc, c->stream3));
         c->launches += 1;
     }
+    if (Q > 0) {
+        RET(launch_query(c, P));
+        c->launches += 1;
+    }
+    if (c->timing) CK(cudaEventRecord(evs[2], c->stream));
+    if (tree) CK(cudaStreamWaitEvent(c->stream, c->ev_tc, 0));
     if (c->timing) {
         CK(cudaEventRecord(evs[3], c->stream));
         c->ev_pending.push_back(evs);

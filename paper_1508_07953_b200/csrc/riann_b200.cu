@@ -413,6 +413,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d_bps, dk, 256, 0));
     const unsigned d_grid = (unsigned)(c->sms * std::max(d_bps, 1));
     // first anchors (search.py:119-133): the draw kernel seeds each key's generator
+    CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));  // the draw counts anchors
     dk<<<d_grid, 256, 0, c->stream>>>(B, 1);
     CK(cudaGetLastError());
     c->launches += 1;
@@ -446,9 +447,6 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         }
         CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
         CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
-        CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
-        rb::bulk_count_kernel<<<small_grid, 256, 0, c->stream>>>(B);
-        CK(cudaGetLastError());
         CK(cub::DeviceScan::ExclusiveSum(c->b_scan_tmp.p, scan_bytes, B.counts, B.starts, (int)(n + 1), c->stream));
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
         rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
@@ -457,6 +455,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaGetLastError());
         fk<<<f_grid, rb::FW2 * 32, fsmem, c->stream>>>(B, ph & 1);
         CK(cudaGetLastError());
+        CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));  // the draw counts anchors
         dk<<<d_grid, 256, 0, c->stream>>>(B, ph & 1);
         CK(cudaGetLastError());
         c->launches += 5;

@@ -1038,6 +1038,7 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
                 rng_store(*sp, rng);
                 status = ST_ACTIVE;
                 P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+                atomicAdd(P.counts + an, 1);  // grouping by anchor for the next phase
             } else if (want) {
                 status = ST_HEAVY;
                 P.heavy[atomicAdd(P.n_heavy, 1)] = (int32_t)g;

@@ -440,14 +440,6 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
     }
 }
 
-// counting sort of the active queries by anchor row
-__global__ void bulk_count_kernel(BulkParams P)
-{
-    const int m = *P.n_active_in;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-        atomicAdd(P.counts + P.st[P.active_in[i]].anchor, 1);
-}
-
 // descriptors of the active queries in anchor order
 __global__ void bulk_scatter_kernel(BulkParams P)
 {

@@ -382,19 +382,36 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                 bool crossed = w0 * 32 >= jh;
                 uint16_t *dst = slot + o + (crossed ? gap : 0);
                 const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
+                if ((jh & 31) == 0) {
+                    // part boundary on a word boundary: one check per word
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    uint32_t word = wd[k];
-                    const uint32_t base = (uint32_t)(w0 + k) * 32u;
-                    while (word) {
-                        const int b = __ffs(word) - 1;
-                        word &= word - 1;
-                        const uint32_t j = base + b;
-                        if (!crossed && (int)j >= jh) {
+                    for (int k = 0; k < 4; k++) {
+                        uint32_t word = wd[k];
+                        const uint32_t base = (uint32_t)(w0 + k) * 32u;
+                        if (!crossed && (int)base >= jh && word) {
                             crossed = true;
                             dst += gap;
                         }
-                        *dst++ = (uint16_t)j;
+                        while (word) {
+                            *dst++ = (uint16_t)(base + (uint32_t)(__ffs(word) - 1));
+                            word &= word - 1;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        uint32_t word = wd[k];
+                        const uint32_t base = (uint32_t)(w0 + k) * 32u;
+                        while (word) {
+                            const int b = __ffs(word) - 1;
+                            word &= word - 1;
+                            const uint32_t j = base + b;
+                            if (!crossed && (int)j >= jh) {
+                                crossed = true;
+                                dst += gap;
+                            }
+                            *dst++ = (uint16_t)j;
+                        }
                     }
                 }
             }

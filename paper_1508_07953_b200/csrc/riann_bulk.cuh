@@ -717,13 +717,13 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                     if (qi[k] >= 0) {
                         const int4 d = desc[qi[k]];
                         gq = d.x;
-                        const int lo = d.z & 0x1ffff, hi = d.w & 0x1ffff;
+                        const uint32_t lo = (uint32_t)(d.z & 0x1ffff), wlen = (uint32_t)(d.w & 0x1ffff) - lo;
                         const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
 #pragma unroll
                         for (int x = 0; x < 8; x++) {
                             if ((al[k] >> x) & 1u) {
-                                const int r = rowb[e8[x]];
-                                if (r >= lo && r < hi) keep |= 1u << x;
+                                const uint32_t r = rowb[e8[x]];
+                                if (r - lo < wlen) keep |= 1u << x;  // lo <= r < hi
                             }
                         }
                         bnxt[eb[k] >> 3] = (uint8_t)keep;

@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                     mbar_wait(&rbar, rpar);
                     rpar ^= 1;
                 }
-                const uint16_t *rowb = row - (int64_t)h * jh;  // indexed by j
+                const uint32_t hoff = (uint32_t)(h * jh), jmax = (uint32_t)(jh - 1);
 #pragma unroll
                 for (int k = 0; k < NPRE; k++) {
                     if (k * FW2 * 32 >= NG) break;  // block-uniform
@@ -719,13 +719,15 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                         gq = d.x;
                         const uint32_t lo = (uint32_t)(d.z & 0x1ffff), wlen = (uint32_t)(d.w & 0x1ffff) - lo;
                         const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
+                        // all eight lookups issued unconditionally (padding / dead entries
+                        // clamped into the half row), the alive bits mask the result
+                        uint32_t rk[8];
 #pragma unroll
-                        for (int x = 0; x < 8; x++) {
-                            if ((al[k] >> x) & 1u) {
-                                const uint32_t r = rowb[e8[x]];
-                                if (r - lo < wlen) keep |= 1u << x;  // lo <= r < hi
-                            }
-                        }
+                        for (int x = 0; x < 8; x++) rk[x] = row[min((uint32_t)e8[x] - hoff, jmax)];
+#pragma unroll
+                        for (int x = 0; x < 8; x++)
+                            keep |= (rk[x] - lo < wlen ? 1u : 0u) << x;  // lo <= r < hi
+                        keep &= al[k];
                         bnxt[eb[k] >> 3] = (uint8_t)keep;
                     }
                     const int q_l0 = __shfl_sync(FULL, qi[k], 0);

@@ -44,10 +44,10 @@
 #define RIANN_P0A_MINB 3
 #endif
 #ifndef RIANN_FILTER_MINB
-#define RIANN_FILTER_MINB 2
+#define RIANN_FILTER_MINB 3
 #endif
 #ifndef RIANN_FILTER_LCAP
-#define RIANN_FILTER_LCAP 16384
+#define RIANN_FILTER_LCAP 8192
 #endif
 #ifndef RIANN_WIN_MINB
 #define RIANN_WIN_MINB 4
@@ -61,7 +61,10 @@ namespace rb {
 constexpr int LIGHT_MAX = 32752;  // largest first ring handled by the bulk path (u16 list positions)
 constexpr int BULK_U = 8;        // used anchors tracked per query (prev + 7 draws at max_rings = 8)
 constexpr int COARSE = 64;       // coarse index stride of the sorted rows
-constexpr int FCAP = 256;        // query descriptors per filter stage
+#ifndef RIANN_FCAP
+#define RIANN_FCAP 248  // three filter CTAs (64 KB half row each) fit an SM
+#endif
+constexpr int FCAP = RIANN_FCAP;  // query descriptors per filter stage
 #ifndef RIANN_FILTER_WARPS
 #define RIANN_FILTER_WARPS 16
 #endif

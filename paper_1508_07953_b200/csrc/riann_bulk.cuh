@@ -570,8 +570,12 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
     };
     // work items: batches of FGRAB consecutive (anchor, half) items taken with
     // one atomic; warp 1 reads a batch's counts / starts in one load round into
-    // a lane window, so only one item in FGRAB waits on memory
-    constexpr int FGRAB = 16;
+    // a lane window, so only one item in FGRAB waits on memory (8: measured
+    // best of 8 / 16 / 32)
+#ifndef RIANN_FGRAB
+#define RIANN_FGRAB 8
+#endif
+    constexpr int FGRAB = RIANN_FGRAB;
     const int nitems = (int)(2 * n);
     int win_it = -1, win_cnt = 0, win_start = 0;  // per lane of warp 1
     unsigned win_mask = 0;

@@ -2,27 +2,28 @@
 //
 // The per-query kernel (K2) pays one random DRAM fetch (~64 B) per ring
 // membership test: ~5,000 tests per query at config 3.  Here the frame runs in
-// phases instead:
-//   P0   (warp per query): exact d_prev, first-ring window (coarse + fine
-//        search), the window as an ascending fixed list (np.sort,
-//        search.py:116) split in two parts (j < n/2, j >= n/2, each padded to 8
-//        entries) with an alive bitmap, first anchor draw (numpy RNG), exact
-//        d_a and the anchor's window.
+// phases instead, all in query-independent bulk steps:
+//   P0a  (eight lanes per query): exact d_prev, first-ring window (level-1 /
+//        coarse / row search), list allocation (search.py:114-117).
+//   P0b  (warp per query): the window as an ascending fixed list (np.sort,
+//        search.py:116) split in two parts (j < n/2, j >= n/2, each padded to
+//        8 entries) with an alive bitmap.
+//   draw (eight lanes per query): |S'|, empty-intersection rollback
+//        (search.py:136-137), next anchor avail[k] (search.py:122-130) selected
+//        over the alive bits with the key's numpy generator; counts anchors.
 //   ring phase k (<= max_rings-1 times):
-//     group    the active queries are counting-sorted by anchor; each gets a
-//              16-byte descriptor in anchor order.
-//     filter   (CTA per (anchor, half-row) work item): TMA copies the anchor's
-//              half rank row pos[a][*] (n bytes) and the descriptors of every
-//              query that drew it into shared memory; the warps share the
-//              queries' list segments (256 entries) and write the new alive
-//              bits: lo <= pos[a][j] < hi is exactly the searchsorted window
-//              test of search.py:77-79, 133-134.  Every anchor row is read
-//              from HBM once per phase.
-//     draw     (warp per query): |S'|, empty-intersection rollback
-//              (search.py:136-137), next anchor avail[k] (search.py:122-131)
-//              selected over the alive bits, exact d_a and its window.
-//   F    (warp per query): fp16-screened final scan of S u {prev} with exact
-//        FP64 re-check.
+//     group    queries counting-sorted by anchor, one 16-byte descriptor each.
+//     window   (eight lanes per query, anchor order) exact d_a and the
+//              anchor's window (search.py:131-133).
+//     filter   (CTA per (anchor, half-row) item): one TMA bulk copy of half the
+//              anchor's rank row pos[a][*] (n bytes) into shared memory; the
+//              queries' list groups and alive bytes are loaded into registers;
+//              lo <= pos[a][j] < hi is exactly the searchsorted window test of
+//              search.py:77-79, 133-134.  Every anchor row is read from HBM
+//              once per phase.
+//     draw     as above.
+//   F    (warp per query): fp16 PCA-basis screened final scan of S u {prev}
+//        with exact FP64 re-check (search.py:140-150).
 // A query that does not fit (first ring > LIGHT_MAX, > BULK_U used anchors) is
 // marked heavy and recomputed from scratch by K2, so results never depend on
 // the path taken.
@@ -148,16 +149,6 @@ __device__ __forceinline__ void seed_frame(Pcg64 &rng, const BulkParams &P, int6
     pcg_seed(rng, fw, P.seed_nw + 3);
 }
 
-__device__ __forceinline__ void rng_load(Pcg64 &r, const QState &s)
-{
-    r.sh = s.sh;
-    r.sl = s.sl;
-    r.ih = s.ih;
-    r.il = s.il;
-    r.has = s.rng_has;
-    r.buf = s.rng_buf;
-}
-
 __device__ __forceinline__ void rng_store(QState &s, const Pcg64 &r)
 {
     s.sh = r.sh;
@@ -168,118 +159,10 @@ __device__ __forceinline__ void rng_store(QState &s, const Pcg64 &r)
     s.rng_buf = r.buf;
 }
 
-// searchsorted pair on a sorted row through its coarse index: returns
-// lo = first v >= lv and hi = first v > hv.  The coarse array (shared or global
-// memory) is searched 17-ary by the two half-warps (as ring_window); the
-// remaining <= 65 entries of the row are counted.
-__device__ __forceinline__ void window_coarse(const float *__restrict__ row, const float *cs, int nb, int64_t n,
-                                              double lv, double hv, int lane, int64_t &lo, int64_t &hi)
-{
-    const int h = lane >> 4, hl = lane & 15;
-    const double thr = h ? hv : lv;
-    int b0 = 0, b1 = nb;  // first coarse entry failing the predicate lies in [b0, b1]
-    for (;;) {
-        const int s = b1 - b0;
-        if (!__any_sync(FULL, s > 16)) break;
-        const int p = b0 + (int)(((int64_t)(hl + 1) * s) / 17);
-        bool pr = false;
-        if (s > 16) {
-            const double v = (double)cs[p];
-            pr = h ? (v <= thr) : (v < thr);
-        }
-        const unsigned ball = __ballot_sync(FULL, pr);
-        const int c = __popc((ball >> (h * 16)) & 0xffffu);
-        const int p_lo = __shfl_sync(FULL, p, h * 16 + (c > 0 ? c - 1 : 0));
-        const int p_hi = __shfl_sync(FULL, p, h * 16 + (c < 16 ? c : 15));
-        if (s > 16) {
-            if (c > 0) b0 = p_lo + 1;
-            if (c < 16) b1 = p_hi;
-        }
-    }
-    {
-        const int p = b0 + hl;
-        bool pr = false;
-        if (p < b1) {
-            const double v = (double)cs[p];
-            pr = h ? (v <= thr) : (v < thr);
-        }
-        const unsigned ball = __ballot_sync(FULL, pr);
-        b0 += __popc((ball >> (h * 16)) & 0xffffu);
-    }
-    const int b = b0;  // coarse entries [0, b) satisfy the predicate
-    const int64_t s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
-    const int64_t s1 = (b < nb) ? (int64_t)b * COARSE : n;
-    int cnt = 0;
-    for (int64_t k = s0 + hl; k < s1; k += 16) {
-        const double v = (double)__ldg(row + k);
-        cnt += (h ? (v <= thr) : (v < thr)) ? 1 : 0;
-    }
-#pragma unroll
-    for (int o = 1; o < 16; o <<= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-    const int64_t res = s0 + cnt;
-    lo = __shfl_sync(FULL, res, 0);
-    hi = __shfl_sync(FULL, res, 16);
-}
-
-// exact d_a (search.py:131, numpy order) and the anchor's window on its sorted
-// row (search.py:133 via :77-79), whole warp
-template <int D>
-__device__ __forceinline__ void anchor_window(const BulkParams &P, int a, const float *q, int lane, int &lo, int &hi)
-{
-    const double da = exact_dist_all<D>(P.refs, a, q, D, lane);
-    int64_t l, h;
-    window_coarse(P.sdist + (int64_t)a * P.n, P.coarse + (int64_t)a * P.ncoarse, P.ncoarse, P.n,
-                  __dsub_rn(da, __dmul_rn(P.alpha, da)), __dadd_rn(da, __dmul_rn(P.alpha, da)), lane, l, h);
-    lo = (int)l;
-    hi = (int)h;
-}
-
-// k-th (0-based) element of ascending list S minus the used anchors u[0..nu)
-// (search.py:122, 129).  upos: positions of the used anchors in S.
-__device__ __forceinline__ int avail_pos(int k, const int *upos, int nu)
-{
-    int pos = k;
-    for (int it = 0; it <= nu; it++) {
-        int c = 0;
-        for (int i = 0; i < nu; i++) c += upos[i] <= pos ? 1 : 0;
-        if (k + c == pos) break;
-        pos = k + c;
-    }
-    return pos;
-}
-
-// List position of the k-th (0-based) alive entry that is not a used anchor
-// (avail[k], search.py:122, 129); bw: the query's alive-bit words, up/ua: used
-// anchor positions and which of them are alive.  Whole warp.
-__device__ __forceinline__ int select_avail(const uint32_t *bw, int nwords, const uint16_t (&up)[BULK_U], int nu,
-                                            int k, int lane)
-{
-    int run = 0;
-    for (int w0 = 0; w0 < nwords; w0 += 32) {
-        const int wi = w0 + lane;
-        uint32_t word = wi < nwords ? bw[wi] : 0u;
-#pragma unroll
-        for (int u = 0; u < BULK_U; u++)
-            if (u < nu && (up[u] >> 5) == wi) word &= ~(1u << (up[u] & 31));
-        const int c = __popc(word);
-        const int inc = warp_incl_scan(c, lane);
-        const int tot = __shfl_sync(FULL, inc, 31);
-        if (k < run + tot) {
-            const int ex = run + inc - c;
-            int pos = -1;
-            if (k >= ex && k < ex + c) pos = wi * 32 + (int)__fns(word, 0u, k - ex + 1);
-            const unsigned b = __ballot_sync(FULL, pos >= 0);
-            return __shfl_sync(FULL, pos, __ffs(b) - 1);
-        }
-        run += tot;
-    }
-    return -1;
-}
-
 __device__ __forceinline__ int bit_at(const uint8_t *bits, int64_t e) { return (bits[e >> 3] >> (e & 7)) & 1; }
 
 // ---------------------------------------------------------------------------
-// P0: first ring, fixed candidate list, first anchor.  One warp per query.
+// P0b: the first ring as a fixed ascending candidate list.  One warp per query.
 // The first-ring window (unordered: distance order) becomes the ascending
 // candidate list (np.sort, search.py:116) through a per-warp n-bit bitmap in
 // shared memory, enumerated word-interleaved: at step t lane L takes words

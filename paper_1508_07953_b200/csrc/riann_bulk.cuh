@@ -1135,7 +1135,10 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
             };
             int nA = 0;
             // FU rounds of 16 candidates per iteration, their loads issued together
-            constexpr int FU = 4;
+#ifndef RIANN_FINAL_FU
+#define RIANN_FINAL_FU 4
+#endif
+            constexpr int FU = RIANN_FINAL_FU;
             for (int e0 = 0; e0 < bn; e0 += 16 * FU) {
                 uint4 v[FU];
                 uint32_t jj[FU];

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define RIANN_ABI_VERSION 1
+#define RIANN_ABI_VERSION 2
 
 enum {
     RIANN_OK = 0,
@@ -80,6 +80,20 @@ uint64_t riann_ctx_device_bytes(riann_ctx *ctx);
  * All paths produce identical results; the switch exists for testing. */
 int riann_ctx_set_path(riann_ctx *ctx, int path);
 
+/* ---- stream slots ------------------------------------------------------ */
+/* The device-resident stream state (previous field, previous frame's unit
+ * rows, replay snapshot) lives in a slot; the context has one active slot
+ * (0 at creation) and keeps the others parked.  The reference's
+ * stream_fields (engine.py:205-227) is a generator with no shared state, so
+ * every stream (a clip, a row band) selects its own slot before
+ * riann_process_frame: interleaved streams on one GPU never read each
+ * other's field or units.  Selecting an unknown slot creates it empty;
+ * freeing the active slot empties it and selects slot 0.  A model upload
+ * invalidates every slot's field and units. */
+int riann_slot_select(riann_ctx *ctx, int slot);
+int riann_slot_current(riann_ctx *ctx);
+int riann_slot_free(riann_ctx *ctx, int slot);
+
 /* ---- model (model.py:56-83 ReferenceModel) ----------------------------- */
 /* refs: (n, dim) float32 unit rows; patch (pw, ph); channels; metric_id must
  * be 0 (Euclidean, patches.py:164-179).  dim must equal pw*ph*channels. */
@@ -123,6 +137,13 @@ int riann_timing_read(riann_ctx *ctx, double *ms3, uint64_t *frames, uint64_t *l
  * previous units), e.g. to replay the same frames; one snapshot per context. */
 int riann_state_save(riann_ctx *ctx);
 int riann_state_restore(riann_ctx *ctx);
+/* Per-position temporal-change terms ||unit_t[g] - unit_{t-1}[g]|| (float64)
+ * of the last RIANN_F_TEMPORAL frame on this context (engine.py:163-171
+ * before its sum), so that row bands can be summed in numpy's pairwise order
+ * over the whole frame.  Valid until the next riann_process_frame on the
+ * context; flags may hold RIANN_F_DEVICE_PTRS (out on the ctx device, no
+ * synchronisation). */
+int riann_tc_get(riann_ctx *ctx, double *out, int64_t count, unsigned flags);
 /* Read back the device-resident field of the last frame. */
 int riann_field_get(riann_ctx *ctx, int32_t *idx, double *dist, int64_t count);
 

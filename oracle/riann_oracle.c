@@ -40,14 +40,49 @@ double rno_pairwise_sum(const double *a, int64_t n)
     return rno_pairwise_sum(a, h) + rno_pairwise_sum(a + h, n - h);
 }
 
+/* rno_pairwise_sum over the squared differences (f64(r_i) - f64(q_i))^2,
+ * each term formed on the fly: the same individually rounded operations in
+ * the same order as squaring into a buffer first (numpy's d = r - q; d * d;
+ * np.sum), without the buffer round trip. */
+static double pw_sq(const float *q, const float *r, int64_t n)
+{
+    if (n < 8) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            double d = (double)r[i] - (double)q[i];
+            s += d * d;
+        }
+        return s;
+    }
+    if (n <= 128) {
+        double acc[8];
+        for (int j = 0; j < 8; j++) {
+            double d = (double)r[j] - (double)q[j];
+            acc[j] = d * d;
+        }
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) {
+                double d = (double)r[i + j] - (double)q[i + j];
+                acc[j] += d * d;
+            }
+        double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        for (; i < n; i++) {
+            double d = (double)r[i] - (double)q[i];
+            s += d * d;
+        }
+        return s;
+    }
+    int64_t h = n / 2;
+    h -= h % 8;
+    return pw_sq(q, r, h) + pw_sq(q + h, r + h, n - h);
+}
+
 /* patches.py:151-159 */
 static double sq_dist(const float *q, const float *r, int dim, double *tmp)
 {
-    for (int i = 0; i < dim; i++) {
-        double d = (double)r[i] - (double)q[i];
-        tmp[i] = d * d;
-    }
-    return sqrt(rno_pairwise_sum(tmp, dim));
+    (void)tmp;
+    return sqrt(pw_sq(q, r, dim));
 }
 
 void rno_one_to_many(const float *q, const float *refs, const int64_t *rows,
@@ -173,11 +208,6 @@ static void pool_run(int nthreads, int64_t count, int64_t chunk,
 
 /* ------------------------------------------------------------------------ */
 /* model.py:162-189 compute_sorted_lists */
-static int cmp_u64(const void *a, const void *b)
-{
-    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
-    return (x > y) - (x < y);
-}
 
 typedef struct {
     const float *refs;
@@ -198,7 +228,7 @@ static void *sorted_mk(void *c)
     sorted_ctx *s = (sorted_ctx *)c;
     sorted_scratch *k = (sorted_scratch *)malloc(sizeof(*k));
     k->tmp = (double *)malloc(sizeof(double) * (size_t)s->dim);
-    k->keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)s->n);
+    k->keys = (uint64_t *)malloc(sizeof(uint64_t) * 2 * (size_t)s->n);
     return k;
 }
 
@@ -223,7 +253,22 @@ static void build_row(const float *refs, int64_t n, int dim, int64_t i, float *d
          * the low word makes the order the stable argsort's */
         keys[j] = ((uint64_t)bits << 32) | (uint64_t)j;
     }
-    qsort(keys, (size_t)n, sizeof(uint64_t), cmp_u64);
+    /* stable LSD radix sort on the float bits (keys start in index order, so
+     * equal distances keep ascending indices: argsort(kind='stable')) */
+    {
+        uint64_t *src = keys, *dst = keys + n;
+        for (int shift = 32; shift < 64; shift += 16) {
+            int64_t *cnt = (int64_t *)calloc(65537, sizeof(int64_t));
+            for (int64_t j = 0; j < n; j++) cnt[((src[j] >> shift) & 0xffff) + 1]++;
+            for (int b = 0; b < 65536; b++) cnt[b + 1] += cnt[b];
+            for (int64_t j = 0; j < n; j++) dst[cnt[(src[j] >> shift) & 0xffff]++] = src[j];
+            free(cnt);
+            uint64_t *t = src;
+            src = dst;
+            dst = t;
+        }
+        /* two passes: the sorted keys are back in keys[0..n) */
+    }
     int64_t self = 0;
     while ((int64_t)(uint32_t)keys[self] != i) self++;
     if (self != 0) { /* duplicates of i sort ahead of it: self goes first */
@@ -423,7 +468,7 @@ static void *query_mk_n(int64_t n, int dim)
     s->mark = (unsigned char *)calloc((size_t)n, 1);
     s->dtmp = (double *)malloc(sizeof(double) * (size_t)dim);
     s->dists = (double *)malloc(sizeof(double) * (size_t)(n + 1));
-    s->keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n);
+    s->keys = (uint64_t *)malloc(sizeof(uint64_t) * 2 * (size_t)n);
     return s;
 }
 
@@ -649,7 +694,13 @@ int rno_query_positions(const rno_model *m, const float *units,
 {
     pos_ctx c = {m, units, prev, positions, gw, seed, t, L, max_rings, alpha,
                  out_idx, out_dist, out_rings, out_evals, out_cand, out_first, 0};
-    pool_run(nthreads, count, 64, pos_run, &c, pos_mk, query_fr);
+    /* chunks of ceil(count / (4 * threads)) positions (at most 64): every
+     * thread gets work even for a few hundred positions */
+    {
+        int64_t nt = nthreads < 1 ? 1 : nthreads, ch = (count + 4 * nt - 1) / (4 * nt);
+        if (ch > 64) ch = 64;
+        pool_run(nthreads, count, ch, pos_run, &c, pos_mk, query_fr);
+    }
     return c.err;
 }
 
@@ -713,6 +764,10 @@ int rno_exact_nn_batch(const float *refs, int64_t n, int dim,
                        int32_t *idx, double *dist)
 {
     enn_ctx c = {refs, queries, n, dim, idx, dist};
-    pool_run(nthreads, count, 8, enn_run, &c, NULL, NULL);
+    {
+        int64_t nt = nthreads < 1 ? 1 : nthreads, ch = (count + 4 * nt - 1) / (4 * nt);
+        if (ch > 8) ch = 8;
+        pool_run(nthreads, count, ch, enn_run, &c, NULL, NULL);
+    }
     return 0;
 }

@@ -50,6 +50,9 @@ SIGNATURES = {
     "riann_sync": (i32, [P]),
     "riann_ctx_device_bytes": (u64, [P]),
     "riann_ctx_set_path": (i32, [P, i32]),
+    "riann_slot_select": (i32, [P, i32]),
+    "riann_slot_current": (i32, [P]),
+    "riann_slot_free": (i32, [P, i32]),
     "riann_model_set_refs": (i32, [P, P, i64, i32, i32, i32, i32, i32]),
     "riann_model_set_tables": (i32, [P, P, P]),
     "riann_model_build_tables": (i32, [P]),
@@ -58,6 +61,7 @@ SIGNATURES = {
                                   P, P, C.POINTER(FrameStatsC)]),
     "riann_set_prev_units": (i32, [P, P, i64, i32]),
     "riann_field_get": (i32, [P, P, P, i64]),
+    "riann_tc_get": (i32, [P, P, i64, C.c_uint]),
     "riann_state_save": (i32, [P]),
     "riann_state_restore": (i32, [P]),
     "riann_timing_enable": (i32, [P, i32]),
@@ -164,9 +168,42 @@ class Context:
         self.h = h
         self.model_token = None    # object identity of the resident model (refs + sorted tables)
         self.refs_token = None     # object identity of the model whose refs are resident
-        self.field_gen = 0         # generation of the device-resident field
-        self.units_gen = 0         # generation of the device-resident prev units
+        self.model_epoch = 0       # bumped by every model upload (invalidates every slot)
+        self.active_slot = 0       # stream slot selected on the C side (riann_slot_select)
+        self._next_slot = 1
+        self._slot_gen = {0: 0}    # per-slot generation of the device-resident field
         self.lock = threading.RLock()
+
+    # -- stream slots: one device-resident field + prev units per stream ------
+    def new_slot(self) -> int:
+        with self.lock:
+            s = self._next_slot
+            self._next_slot += 1
+            self._slot_gen[s] = 0
+            return s
+
+    def select(self, slot: int) -> None:
+        """Make ``slot`` the active stream state (caller holds ``lock``)."""
+        if slot != self.active_slot:
+            check(lib().riann_slot_select(self.h, int(slot)))
+            self.active_slot = slot
+
+    def free_slot(self, slot: int) -> None:
+        with self.lock:
+            if self.h and slot in self._slot_gen and slot != 0:
+                check(lib().riann_slot_free(self.h, int(slot)))
+                del self._slot_gen[slot]
+                if self.active_slot == slot:
+                    self.active_slot = 0
+
+    def advance(self, slot: int) -> tuple:
+        """A new field was produced in ``slot``: bump and return its token."""
+        self._slot_gen[slot] = self._slot_gen.get(slot, 0) + 1
+        return self.token(slot)
+
+    def token(self, slot: int) -> tuple:
+        """Identity of the field currently resident in ``slot``."""
+        return (id(self), slot, self.model_epoch, self._slot_gen.get(slot, -1))
 
     @property
     def stream(self) -> int:

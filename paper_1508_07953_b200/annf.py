@@ -22,7 +22,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .engine import AnnField, FrameStats, _frame_for, _seed_u64, grid_shape, init_field
+from .engine import (AnnField, FrameStats, _device_prev, _frame_for, _restore_units, _seed_u64, grid_shape,
+                     init_field)
 from .errors import DimensionError, FormatError
 from .model import resident
 from .search import SearchParams
@@ -55,12 +56,16 @@ class AnnfWriter:
         self._check(field.width, field.height)
         dev = getattr(field, "_dev", None)
         ctx = N.context() if dev is not None else None
-        if ctx is not None and dev == (id(ctx), ctx.field_gen):
-            payload = np.empty(2 * self.grid_w * self.grid_h, dtype=np.uint32)
+        packed = False
+        if ctx is not None:
             with ctx.lock:
-                N.check(N.lib().riann_field_pack(ctx.h, N.ptr(payload), self.grid_w * self.grid_h))
-            self._f.write(payload.tobytes())
-        else:
+                if _device_prev(ctx, dev[0][1], field):
+                    payload = np.empty(2 * self.grid_w * self.grid_h, dtype=np.uint32)
+                    ctx.select(dev[0][1])
+                    N.check(N.lib().riann_field_pack(ctx.h, N.ptr(payload), self.grid_w * self.grid_h))
+                    self._f.write(payload.tobytes())
+                    packed = True
+        if not packed:
             self._f.write(np.ascontiguousarray(field.indices, dtype="<u4").tobytes())
             self._f.write(np.ascontiguousarray(field.distances, dtype="<f4").tobytes())
         self.frame_count += 1
@@ -130,8 +135,10 @@ def stream_to_annf(model, frames, path, params: SearchParams = SearchParams()):
     stream_fields + AnnfWriter (engine.py:205-227, 257-267).  Returns the
     per-frame FrameStats."""
     ctx = N.context()
+    slot = ctx.new_slot()
     stats = []
     writer = None
+    last_token = last_idx = last_frame = None
     try:
         t = 0
         for frame in frames:
@@ -153,13 +160,19 @@ def stream_to_annf(model, frames, path, params: SearchParams = SearchParams()):
             payload = np.empty(2 * Q, dtype=np.uint32)
             with ctx.lock:
                 resident(ctx, model)
+                ctx.select(slot)
+                if prev is None and last_token != ctx.token(slot):
+                    # another model was uploaded meanwhile: rebuild this stream's state
+                    prev = np.ascontiguousarray(last_idx).reshape(-1)
+                    _restore_units(ctx, slot, model, last_frame)
                 N.check(N.lib().riann_process_frame(
                     ctx.h, N.ptr(f), H, W, Cn, 0, N.ptr(prev), _seed_u64(params.seed), t + 1,
                     int(min(params.L, 2**31 - 1)), float(params.alpha), int(min(params.max_rings, 2**31 - 1)),
                     flags, None, None, C.byref(st)))
-                ctx.field_gen += 1
+                last_token = ctx.advance(slot)
                 N.check(N.lib().riann_field_pack(ctx.h, N.ptr(payload), Q))
             prev = None
+            last_idx, last_frame = payload[:Q].view(np.int32), f
             writer.append_payload(payload)
             stats.append(FrameStats(int(st.total_rings), int(st.total_distance_evals),
                                     float(int(st.sum_cand_final)) / Q,
@@ -170,6 +183,7 @@ def stream_to_annf(model, frames, path, params: SearchParams = SearchParams()):
                                     fallback_queries=int(st.queries_fallback)))
             t += 1
     finally:
+        ctx.free_slot(slot)
         if writer is not None:
             writer.close()
     return stats

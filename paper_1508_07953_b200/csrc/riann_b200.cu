@@ -18,7 +18,9 @@
 #include <type_traits>
 #include <array>
 #include <cstring>
+#include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "riann_b200.h"
@@ -166,6 +168,25 @@ struct PwTree {
     }
 };
 
+// Per-stream device state: the previous field and the previous frame's unit
+// rows (double-buffered) plus the replay snapshot.  A context holds one active
+// slot and parks the others, so interleaved streams on one GPU (bands of one
+// frame, two clips) never read each other's field or units.
+struct StreamState {
+    DevBuf units[2], fld_idx[2], fld_dist, snap_idx, snap_units;
+    int cur_units = 0, cur_fld = 0;
+    bool have_prev_units = false;
+    int64_t prev_units_rows = 0, field_count = -1;
+    int64_t snap_field = -1, snap_units_rows = 0;
+    bool snap_have_units = false, snap_valid = false;
+    void release()
+    {
+        for (DevBuf *b : {&units[0], &units[1], &fld_idx[0], &fld_idx[1], &fld_dist, &snap_idx, &snap_units})
+            b->release();
+        *this = StreamState();
+    }
+};
+
 }  // namespace
 
 struct riann_ctx {
@@ -206,6 +227,10 @@ struct riann_ctx {
     int64_t prev_units_rows = 0;
     int cur_fld = 0;
     int64_t field_count = -1;
+    // stream slots (riann_slot_select): the active slot's state lives in the
+    // members above and below, the others are parked here
+    int slot = 0;
+    std::map<int, StreamState> parked;
     PwTree tree;
     // state snapshot (riann_state_save / riann_state_restore)
     DevBuf snap_idx, snap_units;
@@ -235,13 +260,38 @@ struct riann_ctx {
         CK(cudaSetDevice(device));
         return 0;
     }
+    // exchange the active stream state with `o`
+    void swap_state(StreamState &o)
+    {
+        for (int k = 0; k < 2; k++) {
+            std::swap(units[k], o.units[k]);
+            std::swap(fld_idx[k], o.fld_idx[k]);
+        }
+        std::swap(fld_dist, o.fld_dist);
+        std::swap(snap_idx, o.snap_idx);
+        std::swap(snap_units, o.snap_units);
+        std::swap(cur_units, o.cur_units);
+        std::swap(cur_fld, o.cur_fld);
+        std::swap(have_prev_units, o.have_prev_units);
+        std::swap(prev_units_rows, o.prev_units_rows);
+        std::swap(field_count, o.field_count);
+        std::swap(snap_field, o.snap_field);
+        std::swap(snap_units_rows, o.snap_units_rows);
+        std::swap(snap_have_units, o.snap_have_units);
+        std::swap(snap_valid, o.snap_valid);
+    }
     uint64_t bytes() const
     {
         uint64_t b = refs.cap + refs16.cap + err16.cap + dmat.cap + pos.cap + coarse.cap + coarse1.cap + b_state.cap + pca_T.cap +
                      refs_pca16.cap + e16p.cap + units_pca.cap +
                      b_pool.cap + sdist.cap + sidx.cap + frame.cap + units[0].cap + units[1].cap + prev.cap +
                      fld_idx[0].cap + fld_idx[1].cap + fld_dist.cap + tc.cap + overflow.cap + keys.cap + x_B.cap + x_A.cap +
-                     x_cand.cap + x_lb.cap;
+                     x_cand.cap + x_lb.cap + snap_idx.cap + snap_units.cap;
+        for (const auto &kv : parked) {
+            const StreamState &st = kv.second;
+            b += st.units[0].cap + st.units[1].cap + st.fld_idx[0].cap + st.fld_idx[1].cap + st.fld_dist.cap +
+                 st.snap_idx.cap + st.snap_units.cap;
+        }
         return b;
     }
 };
@@ -878,6 +928,8 @@ int riann_ctx_destroy(riann_ctx *c)
                       &c->x_idx, &c->x_dist, &c->fx_frame, &c->fx_idx, &c->fx_pay, &c->fx_norm, &c->fx_out,
                       &c->fx_rgb, &c->pack};
     for (DevBuf *b : bufs) b->release();
+    for (auto &kv : c->parked) kv.second.release();
+    c->parked.clear();
     for (auto &a : c->ev_pending)
         for (auto e : a) cudaEventDestroy(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -918,6 +970,47 @@ int riann_ctx_set_path(riann_ctx *c, int path)
     return 0;
 }
 
+int riann_slot_select(riann_ctx *c, int slot)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (slot < 0) return fail(RIANN_E_VALUE, "slot must be >= 0, got %d", slot);
+    if (slot == c->slot) return 0;
+    RET(c->use());
+    CK(cudaStreamSynchronize(c->stream));
+    StreamState cur;
+    c->swap_state(cur);  // active -> cur, active becomes empty
+    c->parked[c->slot] = std::move(cur);
+    auto it = c->parked.find(slot);
+    if (it != c->parked.end()) {
+        c->swap_state(it->second);
+        c->parked.erase(it);
+    }
+    c->slot = slot;
+    return 0;
+}
+
+int riann_slot_current(riann_ctx *c) { return c ? c->slot : -1; }
+
+int riann_slot_free(riann_ctx *c, int slot)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    RET(c->use());
+    CK(cudaStreamSynchronize(c->stream));
+    if (slot == c->slot) {
+        StreamState cur;
+        c->swap_state(cur);
+        cur.release();
+        if (slot != 0) RET(riann_slot_select(c, 0));
+        return 0;
+    }
+    auto it = c->parked.find(slot);
+    if (it != c->parked.end()) {
+        it->second.release();
+        c->parked.erase(it);
+    }
+    return 0;
+}
+
 int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, int pw, int ph, int channels,
                          int metric_id)
 {
@@ -954,6 +1047,12 @@ int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, in
     c->C = channels;
     c->field_count = -1;
     c->have_prev_units = false;
+    c->snap_valid = false;
+    for (auto &kv : c->parked) {
+        kv.second.field_count = -1;
+        kv.second.have_prev_units = false;
+        kv.second.snap_valid = false;
+    }
     return 0;
 }
 
@@ -1354,6 +1453,19 @@ int riann_field_get(riann_ctx *c, int32_t *idx, double *dist, int64_t count)
     if (idx) CK(cudaMemcpyAsync(idx, c->fld_idx[c->cur_fld].p, (size_t)count * 4, cudaMemcpyDeviceToHost, c->stream));
     if (dist) CK(cudaMemcpyAsync(dist, c->fld_dist.p, (size_t)count * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int riann_tc_get(riann_ctx *c, double *out, int64_t count, unsigned flags)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    if (count < 0 || (size_t)count * 8 > c->tc.cap)
+        return fail(RIANN_E_STATE, "no per-position temporal change of %lld positions", (long long)count);
+    RET(c->use());
+    const bool dev = (flags & RIANN_F_DEVICE_PTRS) != 0;
+    CK(cudaMemcpyAsync(out, c->tc.p, (size_t)count * 8, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       c->stream));
+    if (!dev) CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
 

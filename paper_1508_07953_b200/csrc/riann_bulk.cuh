@@ -555,7 +555,9 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
             const int NGt = s_ng;
             // sub-chunks of GC groups; a query's groups may span sub-chunks
             constexpr int GC = NPRE * FW2 * 32;
+            bool ran = false;  // block-uniform (NGt, first_sub are)
             for (int G0 = 0; G0 < NGt || (first_sub && G0 == 0); G0 += GC) {
+                ran = true;
                 const int NG = min(GC, NGt - G0);
                 // list groups and alive bytes of my groups (independent of the row copy)
                 uint32_t al[NPRE];
@@ -632,6 +634,9 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                 first_sub = false;
                 __syncthreads();
             }
+            // no sub-chunk ran: every warp must have read s_ng / qg0 before
+            // warp 0 rewrites them for the next chunk
+            if (!ran) __syncthreads();
         }
         db ^= 1;
     }

@@ -125,8 +125,7 @@ def _upload_refs_only(ctx: N.Context, model) -> None:
     N.check(N.lib().riann_model_set_refs(ctx.h, N.ptr(refs), n, dim, pw, ph, channels,
                                          int(getattr(model, "metric_id", 0))))
     ctx.refs_token = weakref.ref(model)
-    ctx.field_gen += 1
-    ctx.units_gen += 1
+    ctx.model_epoch += 1
 
 
 def resident_refs(ctx: N.Context, model) -> None:
@@ -171,8 +170,7 @@ def resident(ctx: N.Context, model) -> None:
         N.check(N.lib().riann_model_set_tables(ctx.h, N.ptr(sd32), N.ptr(si)))
     ctx.model_token = weakref.ref(model)
     ctx.refs_token = ctx.model_token
-    ctx.field_gen += 1
-    ctx.units_gen += 1
+    ctx.model_epoch += 1
 
 
 def compute_sorted_lists(refs, metric: Metric = EUCLIDEAN):

@@ -32,6 +32,15 @@ Fixtures:
   golden_cfg1.npz /   configs 1-2: riann_query at a seeded sample of positions
   golden_cfg2.npz     through all 30 frames, exactly as engine.py:137-143
                       calls it (positions are independent).
+  golden_cfg3.npz     the D=192 path (config 3's 1080p RGB clip, first 10
+                      frames): a config-3-shaped reference set cut to n=8,192
+                      (reference compute_sorted_lists), plane-major 192-D unit
+                      rows built with the reference's own extract_patches per
+                      plane + normalize_rows (transforms.py:152-157
+                      precedent), riann_query at 256 seeded
+                      positions through the 10 frames.
+  golden_cfg4x.npz    exact_nn (evaluation.py:24-33) at config 4's shape
+                      (n=262,144, D=64) on 256 positions of the first frame.
 """
 
 from __future__ import annotations
@@ -309,6 +318,82 @@ def gen_vga(cfg_id, model=None, refs=None, npos=256):
     return model, refs
 
 
+def rgb_units(frame, patch, pos):
+    """Plane-major 192-D unit rows of a (H, W, 3) frame at grid positions,
+    built from the reference's extract_patches (one plane at a time, the
+    reference has no colour path) and normalize_rows."""
+    planes = [extract_patches(np.ascontiguousarray(frame[..., c]), patch).values[pos]
+              for c in range(frame.shape[2])]
+    unit, _ = normalize_rows(np.concatenate(planes, axis=1))
+    return unit
+
+
+def gen_cfg3(npos=256, nframes=10, n=8192):
+    from dataclasses import replace
+
+    cfg = replace(W.CONFIGS[3], n_refs=n)
+    refs = W.reference_set(cfg)
+    t0 = time.time()
+    sd, si = compute_sorted_lists(refs)
+    model = ReferenceModel(refs=refs, sorted_dist=sd, sorted_idx=si, patch_size=cfg.patch, channels=3)
+    print(f"cfg3 (n={n}, D=192): table build {time.time() - t0:.1f}s")
+    gw, gh = cfg.grid
+    rng = np.random.default_rng(1003)
+    pos = np.sort(rng.choice(gw * gh, size=npos, replace=False))
+    init = np.random.default_rng(0).integers(0, model.n, size=(gh, gw), dtype=np.int32).ravel()
+    prev = init[pos].copy()
+    params = SearchParams()
+    res = {k: np.empty((nframes, npos), dt) for k, dt in
+           [("idx", np.int32), ("dist", np.float64), ("rings", np.int32),
+            ("evals", np.int64), ("cand", np.int64)]}
+    units = []
+    digests = []
+    t0 = time.time()
+    for t, frame in enumerate(W.iter_clip(cfg, nframes)):
+        digests.append(W.digest(frame))
+        unit = rgb_units(frame, cfg.patch, pos)
+        units.append(unit)
+        for j, g in enumerate(pos):
+            y, x = divmod(int(g), gw)
+            r = riann_query(model, unit[j], int(prev[j]), params,
+                            rng_state=query_rng_key(params.seed, x, y, t + 1))
+            res["idx"][t, j] = r.match_index
+            res["dist"][t, j] = r.match_distance
+            res["rings"][t, j] = r.rings_drawn
+            res["evals"][t, j] = r.distance_evals
+            res["cand"][t, j] = r.candidates_final
+        prev = res["idx"][t].copy()
+    print(f"cfg3: {nframes * npos} queries in {time.time() - t0:.1f}s")
+    save("golden_cfg3.npz", n_refs=np.array(n), positions=pos, init_prev=init[pos],
+         frame_digests=np.array(digests), refs_digest=np.array(W.digest(refs)),
+         table_digest=np.array(W.digest(sd.astype(np.float32), si)),
+         table_rows=np.arange(0, n, 997), table_rows_dist=sd[::997].astype(np.float32),
+         table_rows_idx=si[::997], units=np.array(units), **res)
+
+
+def gen_cfg4x(npos=256):
+    cfg = W.CONFIGS[4]
+    refs = W.reference_set(cfg)
+    frame = next(W.iter_clip(cfg, 1))
+    gw, gh = cfg.grid
+    rng = np.random.default_rng(1004)
+    pos = np.sort(rng.choice(gw * gh, size=npos, replace=False))
+    unit, _ = normalize_rows(extract_patches(frame, cfg.patch).values[pos])
+    # refs-only model (SURVEY §3C): exact_nn reads refs and the metric only
+    model = ReferenceModel(refs=refs, sorted_dist=np.zeros((0, 0)), sorted_idx=np.zeros((0, 0), np.int32),
+                           patch_size=cfg.patch)
+    t0 = time.time()
+    idx, dist = [], []
+    for j in range(npos):
+        i, d = exact_nn(unit[j], model)
+        idx.append(i)
+        dist.append(d)
+    print(f"cfg4 exact_nn: {npos} queries over n={model.n} in {time.time() - t0:.1f}s")
+    save("golden_cfg4x.npz", positions=pos, refs_digest=np.array(W.digest(refs)),
+         frame_digest=np.array(W.digest(frame)), units=unit, idx=np.array(idx, np.int32),
+         dist=np.array(dist))
+
+
 def gen_annf():
     import tempfile
 
@@ -409,6 +494,10 @@ def main():
     for name, fn in steps:
         if only is None or name in only:
             fn()
+    if only is not None and "cfg3" in only:
+        gen_cfg3()
+    if only is not None and "cfg4x" in only:
+        gen_cfg4x()
     if not a.skip_vga and (only is None or "vga" in only):
         model, refs = gen_vga(1)
         gen_vga(2, model, refs)

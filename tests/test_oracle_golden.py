@@ -153,3 +153,58 @@ def test_vga_sampled_positions(oracle_mod, cfg_id):
         assert np.array_equal(r["cand"], g["cand"][t]), t
         prev = r["idx"]
         del ys
+
+
+def _cfg3_golden_setup(g):
+    from dataclasses import replace
+
+    from paper_1508_07953_b200 import workloads as W
+
+    cfg = replace(W.CONFIGS[3], n_refs=int(g["n_refs"]))
+    refs = W.reference_set(cfg)
+    assert W.digest(refs) == str(g["refs_digest"])
+    return W, cfg, refs
+
+
+def test_cfg3_d192_units_and_queries(oracle_mod):
+    """D=192 (config 3's 1080p RGB clip, n=8,192 config-3-shaped reference set):
+    plane-major unit rows and riann_query through 10 frames vs the live
+    reference (search.py:83-151 on transforms.py:152-157-style rows)."""
+    g = load_golden("golden_cfg3.npz")
+    W, cfg, refs = _cfg3_golden_setup(g)
+    sd, si = oracle_mod.sorted_lists(refs)
+    rows = g["table_rows"]
+    assert np.array_equal(sd[rows], g["table_rows_dist"])
+    assert np.array_equal(si[rows], g["table_rows_idx"])
+    assert W.digest(sd, si) == str(g["table_digest"])
+    model = oracle_mod.OracleModel(refs, sd, si)
+    gw, gh = cfg.grid
+    pos = g["positions"]
+    prev = g["init_prev"].copy()
+    for t, frame in enumerate(W.iter_clip(cfg, g["idx"].shape[0])):
+        assert W.digest(frame) == str(g["frame_digests"][t])
+        unit = oracle_mod.normalize_rows(W.patch_rows(frame, cfg.patch, pos // gw, pos % gw))[0]
+        assert np.array_equal(unit, g["units"][t]), t
+        r = oracle_mod.query_positions(model, unit, prev, pos, gw, 0, t + 1)
+        for k in ("idx", "dist", "rings", "evals", "cand"):
+            assert np.array_equal(r[k], g[k][t]), (k, t)
+        prev = r["idx"]
+
+
+def test_cfg4_exact_nn_golden(oracle_mod):
+    """exact_nn (evaluation.py:24-33) at config 4's shape, n=262,144, D=64."""
+    from paper_1508_07953_b200 import workloads as W
+
+    g = load_golden("golden_cfg4x.npz")
+    cfg = W.CONFIGS[4]
+    refs = W.reference_set(cfg)
+    assert W.digest(refs) == str(g["refs_digest"])
+    frame = next(W.iter_clip(cfg, 1))
+    assert W.digest(frame) == str(g["frame_digest"])
+    gw, gh = cfg.grid
+    pos = g["positions"]
+    unit = oracle_mod.normalize_rows(W.patch_rows(frame, cfg.patch, pos // gw, pos % gw))[0]
+    assert np.array_equal(unit, g["units"])
+    idx, dist = oracle_mod.exact_nn_batch(refs, unit)
+    assert np.array_equal(idx, g["idx"])
+    assert np.array_equal(dist, g["dist"])

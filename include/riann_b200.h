@@ -133,6 +133,13 @@ int riann_set_prev_units(riann_ctx *ctx, const float *units, int64_t rows, int d
  * of frames and of kernel launches since enable. */
 int riann_timing_enable(riann_ctx *ctx, int on);
 int riann_timing_read(riann_ctx *ctx, double *ms3, uint64_t *frames, uint64_t *launches);
+/* Per-phase split of the same frames (CUDA events between the phases'
+ * launches on the ctx stream, summed ms): units, p0a, p0b, draw, group,
+ * window, filter, final, tail, query (riann_phase_name(k)).  The same
+ * phases are NVTX ranges ("riann:<phase>") for ncu --nvtx. */
+#define RIANN_NPHASES 10
+int riann_timing_phases(riann_ctx *ctx, double *ms, int nphases);
+const char *riann_phase_name(int k);
 /* Snapshot / restore of the device-resident stream state (previous field and
  * previous units), e.g. to replay the same frames; one snapshot per context. */
 int riann_state_save(riann_ctx *ctx);

@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(REPO, "include"),
            "-o", tmp, os.path.join(CSRC, "riann_b200.cu"),
-           "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+           "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     if os.environ.get("RIANN_HANG_DEBUG"):
         cmd.insert(1, "-DRIANN_HANG_DEBUG")
     for d in os.environ.get("RIANN_NVCC_DEFS", "").split():  # development A/B builds

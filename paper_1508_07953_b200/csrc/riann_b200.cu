@@ -5,11 +5,10 @@
 // launches K1 (units) -> K2 (query) -> pairwise reduction per frame on the
 // context's stream.  No CPU fallback: every compute entry point runs on the
 // GPU or returns an error.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_radix_sort.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>  // K3 table build only (preprocessing)
 
 #include <cstdarg>
 #include <cstdio>
@@ -168,6 +167,12 @@ struct PwTree {
     }
 };
 
+// frame phases timed by riann_timing_phases (RIANN_NPHASES in the header)
+enum { PH_UNITS, PH_P0A, PH_P0B, PH_DRAW, PH_GROUP, PH_WINDOW, PH_FILTER, PH_FINAL, PH_TAIL, PH_QUERY };
+const char *const kPhaseNames[RIANN_NPHASES] = {"riann:units", "riann:p0a", "riann:p0b", "riann:draw",
+                                                "riann:group", "riann:window", "riann:filter", "riann:final",
+                                                "riann:tail", "riann:query"};
+
 // Per-stream device state: the previous field and the previous frame's unit
 // rows (double-buffered) plus the replay snapshot.  A context holds one active
 // slot and parks the others, so interleaved streams on one GPU (bands of one
@@ -208,7 +213,6 @@ struct riann_ctx {
     DevBuf pca_T, refs_pca16, e16p, units_pca, e16max;
     bool pca = false;
     float pca_dq = 0.f, pca_eta = 0.f, pca_e16max = 0.f;
-    cublasHandle_t cublas = nullptr;
     int ncoarse = 0, cs1 = 0;
     bool bulk_disabled = false;
     // K4 tensor-core comparator: split reference operand, norms, per-call scratch
@@ -218,7 +222,7 @@ struct riann_ctx {
     uint64_t x_checked = 0, x_fallback = 0;
     // bulk-path frame buffers
     DevBuf b_state, b_pool, b_bits, b_kept, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_gdesc,
-        b_scan_tmp, overflow2;
+        overflow2;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -242,6 +246,12 @@ struct riann_ctx {
     std::vector<std::array<cudaEvent_t, 4>> ev_pending;
     double t_ms[3] = {0, 0, 0};
     uint64_t t_frames = 0, launches = 0;
+    // per-phase event marks of the frame in flight (label, event) and of the
+    // frames not yet read; summed per label by riann_timing_read
+    std::vector<std::pair<int, cudaEvent_t>> marks;
+    std::vector<std::vector<std::pair<int, cudaEvent_t>>> marks_pending;
+    double t_phase[RIANN_NPHASES] = {};
+    bool nvtx_open = false;
 
     cudaEvent_t ev()
     {
@@ -298,6 +308,25 @@ struct riann_ctx {
 
 namespace {
 
+// Mark the start of a frame phase on the ctx stream: a CUDA event while
+// timing is on (riann_timing_phases) and an NVTX range (ncu --nvtx / nsys).
+// label < 0 closes the last phase.
+void tmark(riann_ctx *c, int label)
+{
+    if (c->nvtx_open) {
+        nvtxRangePop();
+        c->nvtx_open = false;
+    }
+    if (label >= 0) {
+        nvtxRangePushA(kPhaseNames[label]);
+        c->nvtx_open = true;
+    }
+    if (!c->timing) return;
+    cudaEvent_t e = c->ev();
+    cudaEventRecord(e, c->stream);
+    c->marks.push_back({label, e});
+}
+
 template <int D, class IdxT>
 int launch_query_t(riann_ctx *c, rb::QueryParams &P)
 {
@@ -350,10 +379,6 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     RET(c->b_counters.ensure(256));
     RET(c->b_counts.ensure((size_t)(n + 1) * 4));
     RET(c->b_starts.ensure((size_t)(n + 1) * 4));
-    size_t scan_bytes = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, c->b_counts.as<int32_t>(), c->b_starts.as<int32_t>(),
-                                     (int)(n + 1), c->stream));
-    RET(c->b_scan_tmp.ensure(scan_bytes));
     // [0..1] active counts, [2] P0 heavy, [3] item counter, [4..5] pool top, [6] ring heavy
     int32_t *ctr = c->b_counters.as<int32_t>();
     CK(cudaMemsetAsync(ctr, 0, 256, c->stream));
@@ -402,20 +427,25 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.stats = Pq.stats;
     B.err = Pq.err;
 
-    // projection for the final scan (q' = T^T q, cuBLAS SGEMM, pedantic fp32) on a
-    // third stream: it needs only the unit rows, so it overlaps P0 and the rings
+    // projection for the final scan (q' = T^T q, fp32 SIMT GEMM) on a third
+    // stream: it needs only the unit rows, so it overlaps P0 and the rings
     RET(c->units_pca.ensure((size_t)QN * D * 4));
     CK(cudaEventRecord(c->ev_units, c->stream));
     CK(cudaStreamWaitEvent(c->stream3, c->ev_units, 0));
     {
-        CK(cublasSetStream(c->cublas, c->stream3) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
-        const float one = 1.f, zero = 0.f;
-        if (cublasSgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)QN, D, &one, c->pca_T.as<float>(), D, Pq.units,
-                        D, &zero, c->units_pca.as<float>(), D) != CUBLAS_STATUS_SUCCESS)
-            return fail(RIANN_E_CUDA, "cublasSgemm failed");
+        using CF = rb::ProjCfg<D>;
+        const int64_t tiles = (QN + CF::PQ - 1) / CF::PQ;
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, rb::proj_kernel<D>, CF::THREADS, 0));
+        const int64_t grid = std::min<int64_t>(tiles, (int64_t)c->sms * std::max(bps, 1));
+        rb::proj_kernel<D><<<(unsigned)std::max<int64_t>(grid, 1), CF::THREADS, 0, c->stream3>>>(
+            Pq.units, c->pca_T.as<float>(), QN, c->units_pca.as<float>());
+        CK(cudaGetLastError());
         CK(cudaEventRecord(c->ev_proj, c->stream3));
+        c->launches += 1;
     }
     // P0a: d_prev, first-ring windows, list allocation (four queries per warp)
+    tmark(c, PH_P0A);
     {
         auto k = rb::bulk_p0a_kernel<D>;
         int bps = 0;
@@ -444,6 +474,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         c->launches += 1;
     }
     // P0b: sorted fixed lists + alive bits (warp per query, bitmap in shared memory)
+    tmark(c, PH_P0B);
     {
         const int wpb = RIANN_P0_WPB;
         const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
@@ -463,6 +494,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d_bps, dk, 256, 0));
     const unsigned d_grid = (unsigned)(c->sms * std::max(d_bps, 1));
     // first anchors (search.py:119-133): the draw kernel seeds each key's generator
+    tmark(c, PH_DRAW);
     CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));  // the draw counts anchors
     dk<<<d_grid, 256, 0, c->stream>>>(B, 1);
     CK(cudaGetLastError());
@@ -497,20 +529,25 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         }
         CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
         CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
-        CK(cub::DeviceScan::ExclusiveSum(c->b_scan_tmp.p, scan_bytes, B.counts, B.starts, (int)(n + 1), c->stream));
-        CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));
+        tmark(c, PH_GROUP);
+        rb::anchor_scan_kernel<<<1, rb::SCAN_T, 0, c->stream>>>(B.counts, B.starts, (int)(n + 1));
+        CK(cudaGetLastError());
         rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
+        tmark(c, PH_WINDOW);
         wk<<<w_grid, 256, 0, c->stream>>>(B);
         CK(cudaGetLastError());
+        tmark(c, PH_FILTER);
         fk<<<f_grid, rb::FW2 * 32, fsmem, c->stream>>>(B, ph & 1);
         CK(cudaGetLastError());
+        tmark(c, PH_DRAW);
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));  // the draw counts anchors
         dk<<<d_grid, 256, 0, c->stream>>>(B, ph & 1);
         CK(cudaGetLastError());
         c->launches += 5;
     }
     // final scan of the light queries (PCA-basis screening)
+    tmark(c, PH_FINAL);
     {
         CK(cudaStreamWaitEvent(c->stream, c->ev_proj, 0));
         rb::ScreenParams SP;
@@ -535,6 +572,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     // scratch on the main stream, then join the second stream
     Pq.qlist = B.heavy;
     Pq.n_qlist = B.n_heavy;
+    tmark(c, PH_TAIL);
     CK(cudaStreamWaitEvent(c->stream, c->ev_heavy, 0));
     return 1;
 }
@@ -663,7 +701,7 @@ int build_pca(riann_ctx *c, const float *refs_host)
         }
     const double eta = std::sqrt(fro) * 1.01 + 1e-12;
     if (eta > 1e-3) return 0;  // basis too far from orthogonal: skip PCA screening
-    // cuBLAS SGEMM error bound for q' = T^T q, ||q|| <= 1 + 1e-6: per component
+    // fp32 GEMM error bound for q' = T^T q (proj_kernel, any summation order), ||q|| <= 1 + 1e-6: per component
     // gamma_D * sum_k |T_ki q_k| <= gamma_D * ||T_.i|| * ||q||
     const double u = std::ldexp(1.0, -24), gam = D * u / (1.0 - D * u);
     const double dq = gam * std::sqrt((double)D) * std::sqrt(1.0 + eta) * (1.0 + 1e-6) * 1.01 + 1e-12;
@@ -685,11 +723,6 @@ int build_pca(riann_ctx *c, const float *refs_host)
     c->pca_dq = (float)dq;
     c->pca_eta = (float)eta;
     c->pca_e16max = e16m;
-    if (!c->cublas) {
-        if (cublasCreate(&c->cublas) != CUBLAS_STATUS_SUCCESS) return fail(RIANN_E_CUDA, "cublasCreate failed");
-        // no TF32 / emulation: the error bound assumes IEEE fp32 FMA dot products
-        cublasSetMathMode(c->cublas, CUBLAS_PEDANTIC_MATH);
-    }
     c->pca = true;
     return 0;
 }
@@ -917,7 +950,7 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->coarse1, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_gdesc, &c->b_scan_tmp, &c->b_bits, &c->b_kept, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
+                      &c->b_gdesc, &c->b_bits, &c->b_kept, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
                       &c->units_pca, &c->e16max, &c->snap_idx, &c->snap_units, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
@@ -933,7 +966,6 @@ int riann_ctx_destroy(riann_ctx *c)
     for (auto &a : c->ev_pending)
         for (auto e : a) cudaEventDestroy(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    if (c->cublas) cublasDestroy(c->cublas);
     cudaStreamSynchronize(c->stream2);
     cudaStreamSynchronize(c->stream3);
     cudaEventDestroy(c->ev_p0);
@@ -1268,6 +1300,7 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         CK(cudaEventRecord(evs[0], c->stream));
     }
     c->launches += 1;
+    tmark(c, PH_UNITS);
     RET(launch_units(c, d_frame, H, W, C, c->units[us].as<float>(), nullptr,
                      temporal ? c->units[us ^ 1].as<float>() : nullptr, temporal ? c->tc.as<double>() : nullptr));
     // K2: queries
@@ -1323,14 +1356,18 @@ int riann_process_frame(riann_ctx *c, const float *frame, int H, int W, int C, i
         c->launches += 1;
     }
     if (Q > 0) {
+        tmark(c, PH_QUERY);
         RET(launch_query(c, P));
         c->launches += 1;
     }
+    tmark(c, -1);
     if (c->timing) CK(cudaEventRecord(evs[2], c->stream));
     if (tree) CK(cudaStreamWaitEvent(c->stream, c->ev_tc, 0));
     if (c->timing) {
         CK(cudaEventRecord(evs[3], c->stream));
         c->ev_pending.push_back(evs);
+        c->marks_pending.push_back(std::move(c->marks));
+        c->marks.clear();
     }
     if (!dev) {
         if (out_idx) CK(cudaMemcpyAsync(out_idx, d_idx, (size_t)Q * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1375,6 +1412,12 @@ int riann_timing_enable(riann_ctx *c, int on)
     for (auto &a : c->ev_pending)
         for (auto e : a) c->ev_pool.push_back(e);
     c->ev_pending.clear();
+    for (auto &f : c->marks_pending)
+        for (auto &m : f) c->ev_pool.push_back(m.second);
+    c->marks_pending.clear();
+    for (auto &m : c->marks) c->ev_pool.push_back(m.second);
+    c->marks.clear();
+    for (double &x : c->t_phase) x = 0.0;
     c->timing = on != 0;
     c->t_ms[0] = c->t_ms[1] = c->t_ms[2] = 0.0;
     c->t_frames = 0;
@@ -1397,12 +1440,31 @@ int riann_timing_read(riann_ctx *c, double *ms3, uint64_t *frames, uint64_t *lau
         c->t_frames++;
     }
     c->ev_pending.clear();
+    for (auto &f : c->marks_pending) {
+        // the stretch between mark i and mark i+1 belongs to mark i's phase
+        for (size_t i = 0; i + 1 < f.size(); i++) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, f[i].second, f[i + 1].second));
+            if (f[i].first >= 0) c->t_phase[f[i].first] += ms;
+        }
+        for (auto &m : f) c->ev_pool.push_back(m.second);
+    }
+    c->marks_pending.clear();
     if (ms3)
         for (int k = 0; k < 3; k++) ms3[k] = c->t_ms[k];
     if (frames) *frames = c->t_frames;
     if (launches) *launches = c->launches;
     return 0;
 }
+
+int riann_timing_phases(riann_ctx *c, double *ms, int nphases)
+{
+    RET(riann_timing_read(c, nullptr, nullptr, nullptr));
+    for (int k = 0; k < nphases && k < RIANN_NPHASES; k++) ms[k] = c->t_phase[k];
+    return 0;
+}
+
+const char *riann_phase_name(int k) { return (k >= 0 && k < RIANN_NPHASES) ? kPhaseNames[k] : nullptr; }
 
 int riann_state_save(riann_ctx *c)
 {

@@ -1283,6 +1283,150 @@ __global__ void refs_pca_kernel(const float *refs, const float *T, int64_t n, in
     atomicMax(e16max, __float_as_uint(b));
 }
 
+// ---------------------------------------------------------------------------
+// Exclusive scan of the per-anchor counts (n + 1 ints) into starts, counts
+// zeroed for the scatter's cursors: one CTA of 1024 threads, each owning a
+// contiguous run (coalesced through shared memory), a warp-shuffle scan of
+// the run totals.  Replaces a library scan + memset (two launches) per ring
+// phase.
+constexpr int SCAN_T = 1024;
+__global__ void __launch_bounds__(SCAN_T) anchor_scan_kernel(int32_t *counts, int32_t *starts, int m)
+{
+    __shared__ int32_t wsum[SCAN_T / 32];
+    __shared__ int32_t carry_s;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) carry_s = 0;
+    __syncthreads();
+    // tiles of SCAN_T * 4 elements, int4-coalesced per thread
+    for (int base = 0; base < m; base += SCAN_T * 4) {
+        int v[4];
+        const int i0 = base + tid * 4;
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[k] = (i0 + k < m) ? counts[i0 + k] : 0;
+        const int tsum = v[0] + v[1] + v[2] + v[3];
+        int inc = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            int x = wsum[lane];
+            int xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += y;
+            }
+            wsum[lane] = xi - x;  // exclusive warp offsets
+        }
+        __syncthreads();
+        int run = carry_s + wsum[w] + inc - tsum;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (i0 + k < m) {
+                starts[i0 + k] = run;
+                counts[i0 + k] = 0;
+            }
+            run += v[k];
+        }
+        __syncthreads();
+        if (tid == SCAN_T - 1) carry_s = run;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Final-scan projection q' = T^T q (T: D x D, T[k][i] = entry k of basis
+// vector i) for every unit row: a register-tiled SIMT GEMM with fp32 FMAs.
+// Each CTA owns PQ queries x all D outputs; K staged through shared memory in
+// chunks of PK.  Any summation order keeps the screening bound dq
+// (gamma_D * sqrt(D) * ||q||, build_pca) valid.
+template <int D>
+struct ProjCfg {
+    static constexpr int PQ = 64;               // queries per CTA
+    static constexpr int TM = 8;                // queries per thread
+    static constexpr int TN = D == 192 ? 12 : 4;  // outputs per thread
+    static constexpr int THREADS = (PQ / TM) * (D / TN);
+    static constexpr int PK = 32;               // k per stage
+};
+
+template <int D>
+__global__ void __launch_bounds__(ProjCfg<D>::THREADS) proj_kernel(const float *__restrict__ units,
+                                                                   const float *__restrict__ T, int64_t Q,
+                                                                   float *__restrict__ out)
+{
+    using CF = ProjCfg<D>;
+    constexpr int PQ = CF::PQ, TM = CF::TM, TN = CF::TN, PK = CF::PK, NT = CF::THREADS;
+    constexpr int TX = D / TN;  // threads along the outputs
+    __shared__ __align__(16) float us[PK][PQ + 4];  // us[k][q]
+    __shared__ __align__(16) float ts[PK][D];       // ts[k][i]
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    for (int64_t q0 = (int64_t)blockIdx.x * PQ; q0 < Q; q0 += (int64_t)gridDim.x * PQ) {
+        float acc[TM][TN];
+#pragma unroll
+        for (int a = 0; a < TM; a++)
+#pragma unroll
+            for (int b = 0; b < TN; b++) acc[a][b] = 0.f;
+        for (int k0 = 0; k0 < D; k0 += PK) {
+            __syncthreads();
+            // unit tile: PQ rows x PK columns (float4 along k), stored transposed
+            for (int e = tid; e < PQ * PK / 4; e += NT) {
+                const int qq = e / (PK / 4), kk = (e % (PK / 4)) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (q0 + qq < Q) v = *reinterpret_cast<const float4 *>(units + (q0 + qq) * D + k0 + kk);
+                us[kk + 0][qq] = v.x;
+                us[kk + 1][qq] = v.y;
+                us[kk + 2][qq] = v.z;
+                us[kk + 3][qq] = v.w;
+            }
+            for (int e = tid; e < PK * D / 4; e += NT) {
+                const int kk = e / (D / 4), ii = (e % (D / 4)) * 4;
+                *reinterpret_cast<float4 *>(&ts[kk][ii]) =
+                    *reinterpret_cast<const float4 *>(T + (int64_t)(k0 + kk) * D + ii);
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int k = 0; k < PK; k++) {
+                float a[TM], b[TN];
+#pragma unroll
+                for (int x = 0; x < TM; x += 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(&us[k][ty * TM + x]);
+                    a[x] = v.x;
+                    a[x + 1] = v.y;
+                    a[x + 2] = v.z;
+                    a[x + 3] = v.w;
+                }
+#pragma unroll
+                for (int x = 0; x < TN; x += 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(&ts[k][tx * TN + x]);
+                    b[x] = v.x;
+                    b[x + 1] = v.y;
+                    b[x + 2] = v.z;
+                    b[x + 3] = v.w;
+                }
+#pragma unroll
+                for (int i = 0; i < TM; i++)
+#pragma unroll
+                    for (int j = 0; j < TN; j++) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < TM; i++) {
+            const int64_t q = q0 + ty * TM + i;
+            if (q < Q) {
+#pragma unroll
+                for (int x = 0; x < TN; x += 4)
+                    *reinterpret_cast<float4 *>(out + q * D + tx * TN + x) =
+                        make_float4(acc[i][x], acc[i][x + 1], acc[i][x + 2], acc[i][x + 3]);
+            }
+        }
+    }
+}
+
 // rank rows and coarse rows of the sorted tables (built once per model)
 __global__ void pos_scatter_kernel(const uint16_t *sidx, int64_t n, int64_t rows, uint16_t *pos)
 {

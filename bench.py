@@ -52,6 +52,7 @@ sys.path.insert(0, REPO)
 
 from paper_1508_07953_b200 import workloads as W  # noqa: E402
 
+NPH = 10  # RIANN_NPHASES
 METRIC = "query patches/sec per ANNF (1080p RGB, 8x8x3 patches, n=65536)"
 
 
@@ -281,7 +282,7 @@ def bf16_peak():
 
 
 def phase_names(N):
-    return [N.lib().riann_phase_name(k).decode() for k in range(10)]
+    return [N.lib().riann_phase_name(k).decode() for k in range(NPH)]
 
 
 def device_frames_run(N, ctx, frames, y0, t_first, ev_pairs=None):
@@ -556,8 +557,8 @@ def run_ours(a):
         ms3 = (C.c_double * 3)()
         nfr, nl = C.c_uint64(0), C.c_uint64(0)
         N.check(lib.riann_timing_read(ctx.h, ms3, C.byref(nfr), C.byref(nl)))
-        phases = (C.c_double * 10)()
-        N.check(lib.riann_timing_phases(ctx.h, phases, 10))
+        phases = (C.c_double * NPH)()
+        N.check(lib.riann_timing_phases(ctx.h, phases, NPH))
         N.check(lib.riann_timing_enable(ctx.h, 0))
         vfield = np.empty((y1 - y0) * gw, np.int32)
         N.check(lib.riann_field_get(ctx.h, N.ptr(vfield), None, vfield.size))
@@ -632,7 +633,7 @@ def run_ours(a):
     qpath_ms = allmax(ms3[1] / K)
     evals = allsum(sum(s.total_distance_evals for s in fstats)) / allsum(sum(s.queries for s in fstats))
     names = phase_names(N)
-    phase_ms = {names[k].split(":")[1]: allmax(phases[k] / K) for k in range(10) if phases[k] > 0}
+    phase_ms = {names[k].split(":")[1]: allmax(phases[k] / K) for k in range(NPH) if phases[k] > 0}
 
     # ---- CPU baseline: oracle on a sample of the last frame (rank 0, N=1)
     cpu = None

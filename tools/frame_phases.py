@@ -16,6 +16,7 @@ from paper_1508_07953_b200 import _native as N  # noqa: E402
 from paper_1508_07953_b200 import workloads as W  # noqa: E402
 from paper_1508_07953_b200.bands import BandStream  # noqa: E402
 
+NPH = 10  # RIANN_NPHASES
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 25
 cfg = W.CONFIGS[int(os.environ.get("CFG", "3"))]
 frames = list(W.iter_clip(cfg, T))
@@ -25,19 +26,19 @@ gw, gh = cfg.grid
 bs = BandStream(model, gw, gh, 0, gh)
 ctx = bs.ctx
 lib = N.lib()
-names = [lib.riann_phase_name(k).decode().split(":")[1] for k in range(10)]
+names = [lib.riann_phase_name(k).decode().split(":")[1] for k in range(NPH)]
 for t in range(T):
     with ctx.lock:
         N.check(lib.riann_timing_enable(ctx.h, 1))
     idx, dist, st = bs.step(frames[t])
-    ph = (C.c_double * 10)()
+    ph = (C.c_double * NPH)()
     with ctx.lock:
-        N.check(lib.riann_timing_phases(ctx.h, ph, 10))
+        N.check(lib.riann_timing_phases(ctx.h, ph, NPH))
         N.check(lib.riann_timing_enable(ctx.h, 0))
     row = {"t": t + 1, "total": round(sum(ph), 2), "fallback": st.fallback_queries,
            "evals/q": round(st.total_distance_evals / st.queries, 1),
            "first/q": round(st.first_ring_total / st.queries, 1),
            "tests/q": round(st.ring_tests_total / st.queries, 1),
            "exact/q": round(st.exact_evals_total / st.queries, 2)}
-    row.update({names[k]: round(ph[k], 2) for k in range(10) if ph[k] > 0})
+    row.update({names[k]: round(ph[k], 2) for k in range(NPH) if ph[k] > 0})
     print(json.dumps(row), flush=True)

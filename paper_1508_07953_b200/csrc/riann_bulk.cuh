@@ -59,7 +59,7 @@
 
 namespace rb {
 
-constexpr int LIGHT_MAX = 32752;  // largest first ring handled by the bulk path (u16 list positions)
+constexpr int LIGHT_MAX = 65520;  // largest first ring handled by the bulk path (list positions < 65,536 fit u16)
 constexpr int BULK_U = 8;        // used anchors tracked per query (prev + 7 draws at max_rings = 8)
 constexpr int COARSE = 64;       // coarse index stride of the sorted rows
 #ifndef RIANN_FCAP

@@ -1000,8 +1000,26 @@ __global__ void __launch_bounds__(256, RIANN_WIN_MINB) bulk_window_kernel(BulkPa
 // (initially the previous match's exact distance).  Survivors of all chunks
 // whose lower bound can still reach the minimum get the exact FP64 distance
 // (numpy order), so the first minimum (lowest index on ties) is exact.
+// refs_pca16 is chunk-major: the 16-component chunk c of reference j is the
+// 32 bytes at (c * n + j) * 16 halves, so chunk 0 of all references (the
+// chunk every candidate is screened with) is one dense n * 32-byte block
+// that stays L2-resident.
+#ifndef RIANN_PCA_CHUNKMAJOR
+#define RIANN_PCA_CHUNKMAJOR 1
+#endif
+__host__ __device__ __forceinline__ int64_t pca_chunk_off(int64_t j, int c, int64_t n, int D)
+{
+#if RIANN_PCA_CHUNKMAJOR
+    (void)D;
+    return ((int64_t)c * n + j) * 16;
+#else
+    (void)n;
+    return j * D + 16 * c;
+#endif
+}
+
 struct ScreenParams {
-    const __half *refs_pca16;  // (n, D) fp16, PCA order
+    const __half *refs_pca16;  // (n, D) fp16, PCA order, chunk-major (pca_chunk_off)
     const float *e16p;         // per-row bound
     const float *units_pca;    // (Q, D) fp32
     float slack;               // dq + max_r e16p[r] + 1e-12 (chunk rejection)
@@ -1039,6 +1057,12 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
     float *sv_lb = reinterpret_cast<float *>(ws + FB * (8 + 2 * sizeof(FIdx)) + SURV_CAP * 4);
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const uint64_t pol_keep = pol_evict_last();
+#ifndef RIANN_FINAL_LIST_ONCE
+#define RIANN_FINAL_LIST_ONCE 1
+#endif
+#if RIANN_FINAL_LIST_ONCE
+    const uint64_t pol_once = pol_evict_first();
+#endif
     unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
     for (int64_t g = (int64_t)blockIdx.x * wpb + wib; g < P.Q; g += nwarps) {
         const QState &sr = P.st[g];
@@ -1101,7 +1125,11 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                 uint4 v = make_uint4(0u, 0u, 0u, 0u);
                 uint32_t al = 0;
                 if (e0 < Wl) {
+#if RIANN_FINAL_LIST_ONCE
+                    v = ld_once16(reinterpret_cast<const uint4 *>(slot + e0), pol_once);
+#else
                     v = *reinterpret_cast<const uint4 *>(slot + e0);
+#endif
                     al = bq[e0 >> 3];
                 }
                 const int c = __popc(al);
@@ -1151,7 +1179,8 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                 for (int u = 0; u < FU; u++) {
                     const int e = e0 + 16 * u + (lane >> 1);
                     jj[u] = Cj[e < bn ? e : 0];
-                    v[u] = ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)jj[u] * D) + hh, pol_keep);
+                    v[u] = ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + pca_chunk_off(jj[u], 0, P.n, D)) + hh,
+                                     pol_keep);
                 }
 #pragma unroll
                 for (int u = 0; u < FU; u++) {
@@ -1184,7 +1213,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                     const uint32_t j = valid ? Aj[i] : Aj[0];
                     const float s0 = valid ? As[i] : 0.f;
                     const uint4 v =
-                        ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + (int64_t)j * D) + 2 * c + hh, pol_keep);
+                        ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + pca_chunk_off(j, c, P.n, D)) + hh, pol_keep);
                     const float s = __fadd_rn(s0, part(v));
                     if (!last) {
                         const bool keep = valid && s <= thr;
@@ -1273,7 +1302,7 @@ __global__ void refs_pca_kernel(const float *refs, const float *T, int64_t n, in
         double y = 0.0;
         for (int k = 0; k < dim; k++) y = fma((double)T[(int64_t)k * dim + i], (double)r[k], y);
         const __half h = __float2half_rn((float)y);
-        out[j * dim + i] = h;
+        out[(dim % 16 == 0) ? pca_chunk_off(j, i >> 4, n, dim) + (i & 15) : j * dim + i] = h;
         const double dl = (double)__half2float(h) - y;
         acc = __fma_ru(dl, dl, acc);
     }

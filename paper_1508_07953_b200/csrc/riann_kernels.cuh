@@ -334,6 +334,15 @@ __device__ __forceinline__ uint4 ld_keep16(const uint4 *a, uint64_t pol)
                  : "l"(a), "l"(pol));
     return v;
 }
+// streamed once (candidate lists): no L1 allocation, evict first from L2
+__device__ __forceinline__ uint4 ld_once16(const uint4 *a, uint64_t pol)
+{
+    uint4 v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(a), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ float ld_keep(const float *a, uint64_t pol)
 {
     float v;

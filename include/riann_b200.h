@@ -107,6 +107,23 @@ int riann_model_set_tables(riann_ctx *ctx, const float *sorted_dist,
 /* K3: build the sorted tables on the GPU, bit-identical to
  * compute_sorted_lists (model.py:162-189). */
 int riann_model_build_tables(riann_ctx *ctx);
+/* ---- row-sharded tables (config 4: n = 262,144 needs 768 GiB of tables) ---
+ * K3 for rows [row0, row0 + rows) only (a shard; compute_sorted_lists
+ * model.py:177-188 restricted to those rows).  A context holding a partial
+ * range serves as a shard owner; it cannot run frames itself. */
+int riann_model_build_table_rows(riann_ctx *ctx, int64_t row0, int64_t rows);
+/* Device pointers of this context's table rows (sorted distances f32,
+ * sorted indices u16 if n <= 65,536 else i32, index-ordered distances f32)
+ * and the row range they hold. */
+int riann_model_table_ptrs(riann_ctx *ctx, void **sdist, void **sidx, void **dmat, int64_t *row0,
+                           int64_t *rows);
+/* Use nshards row shards as this context's tables: row a lives in shard
+ * a / shard_rows at offset (a % shard_rows) * n.  Shards on other GPUs are
+ * read with NVLink peer loads (peer access is enabled here).  The frame path
+ * then runs the per-query kernel (the anchor-grouped path needs local rank
+ * rows).  The owners must outlive this context's use of the shards. */
+int riann_model_attach_shards(riann_ctx *ctx, int nshards, int64_t shard_rows, void *const *sdist,
+                              void *const *sidx, void *const *dmat);
 /* Download rows [row0, row0+rows) of the sorted tables. */
 int riann_model_get_tables(riann_ctx *ctx, int64_t row0, int64_t rows,
                            float *sorted_dist, int32_t *sorted_idx);

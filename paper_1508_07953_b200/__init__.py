@@ -26,6 +26,7 @@ from .patches import (
     normalize_rows,
     register_metric,
 )
+from .shards import ShardedTables, shard_model
 from .search import QueryResult, SearchParams, query_rng_key, riann_query, riann_query_batch, ring_candidates
 from .modelio import MODEL_MAGIC, MODEL_VERSION, deserialize_model, load_model, model_memory_bytes, save_model, serialize_model
 from .transforms import EffectTable, apply_effect, reconstruct_frame, reconstruction_error, reconstruction_table
@@ -75,6 +76,8 @@ __all__ = [
     "exact_nn_batch",
     "extract_patches",
     "field_exact_oracle",
+    "shard_model",
+    "ShardedTables",
     "frame_units",
     "get_metric",
     "grid_shape",

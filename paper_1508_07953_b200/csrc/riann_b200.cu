@@ -209,6 +209,12 @@ struct riann_ctx {
     bool idx16 = false;  // sorted index table stored as uint16 (n <= 65536)
     DevBuf refs, refs16, err16, sdist, sidx, dmat;
     DevBuf pos, coarse, coarse1;  // rank rows and two-level coarse index (bulk path, n <= 65536)
+    // row-sharded tables (riann_model_attach_shards): device arrays of the
+    // shards' sdist / sidx / dmat base pointers; own_row0/own_rows: the rows
+    // this context's own tables hold
+    int nshards = 0;
+    int64_t shard_rows = 0, own_row0 = 0, own_rows = -1;
+    DevBuf sh_ptrs;
     // PCA screening basis (bulk final scan)
     DevBuf pca_T, refs_pca16, e16p, units_pca, e16max;
     bool pca = false;
@@ -582,10 +588,23 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     P.refs16 = c->refs16.as<__half>();
     P.err16 = c->err16.as<float>();
     P.dmat = c->dmat.as<float>();
+    if (c->nshards > 0) {
+        // row-sharded tables: the per-query kernel reads rows through the shard table
+        const void *const *sp = c->sh_ptrs.as<const void *const>();
+        P.sh_sdist = reinterpret_cast<const float *const *>(sp);
+        P.sh_sidx = sp + c->nshards;
+        P.sh_dmat = reinterpret_cast<const float *const *>(sp + 2 * c->nshards);
+        P.shard_rows = c->shard_rows;
+        P.nshards = c->nshards;
+        P.sdist = nullptr;
+        P.sidx = nullptr;
+        P.dmat = nullptr;
+    }
     int bits = 1;
     while (bits < 31 && ((int64_t)1 << bits) < c->n) bits++;
     P.passes = (bits + 7) / 8;
-    if (!P.qlist && !P.key_words && !P.scanned && c->idx16 && c->pos.p && c->pca && !c->bulk_disabled &&
+    if (!P.qlist && !P.key_words && !P.scanned && c->nshards == 0 && c->idx16 && c->pos.p && c->pca &&
+        !c->bulk_disabled &&
         (c->dim == 64 || c->dim == 192) && c->n % 16 == 0) {
         int r = c->dim == 64 ? run_bulk_t<64>(c, P) : run_bulk_t<192>(c, P);
         if (r != 1) return r;
@@ -950,7 +969,7 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->coarse1, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_gdesc, &c->b_bits, &c->b_kept, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p,
+                      &c->b_gdesc, &c->b_bits, &c->b_kept, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p, &c->sh_ptrs,
                       &c->units_pca, &c->e16max, &c->snap_idx, &c->snap_units, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,
@@ -1058,6 +1077,8 @@ int riann_model_set_refs(riann_ctx *c, const float *refs, int64_t n, int dim, in
     c->sdist.release();
     c->sidx.release();
     c->dmat.release();
+    c->nshards = 0;
+    c->own_rows = -1;
     c->pos.release();
     c->coarse.release();
     c->coarse1.release();
@@ -1124,16 +1145,19 @@ int riann_model_set_tables(riann_ctx *c, const float *sd, const int32_t *si)
     }
     stage.release();
     RET(build_bulk_tables(c));
+    c->nshards = 0;
+    c->own_row0 = 0;
+    c->own_rows = n;
     c->tables = true;
     return 0;
 }
 
-int riann_model_build_tables(riann_ctx *c)
+// K3 for table rows [row_lo, row_lo + nrows): sorted rows, index rows and the
+// index-ordered distance rows, stored from row_lo on (a shard holds a row range)
+int build_table_rows(riann_ctx *c, int64_t row_lo, int64_t nrows)
 {
-    RET(check_model(c, false));
-    RET(c->use());
     const int64_t n = c->n;
-    const size_t tcnt = (size_t)n * n;
+    const size_t tcnt = (size_t)nrows * n;
     c->idx16 = n <= 65536;
     RET(c->sdist.ensure(tcnt * 4));
     RET(c->sidx.ensure(tcnt * (c->idx16 ? 2 : 4)));
@@ -1159,8 +1183,10 @@ int riann_model_build_tables(riann_ctx *c)
                                                  d_off.as<int>(), d_off.as<int>() + 1, 0, 32, c->stream));
     DevBuf temp;
     RET(temp.ensure(temp_bytes));
-    for (int64_t r0 = 0; r0 < n; r0 += rb_rows) {
-        const int64_t rows = (r0 + rb_rows <= n) ? rb_rows : n - r0;
+    const int64_t row_hi = row_lo + nrows;
+    for (int64_t r0 = row_lo; r0 < row_hi; r0 += rb_rows) {
+        const int64_t rows = (r0 + rb_rows <= row_hi) ? rb_rows : row_hi - r0;
+        const size_t ro = (size_t)(r0 - row_lo) * n;  // storage offset of row r0
         const unsigned blocks = (unsigned)std::min<int64_t>((rows + 7) / 8, (int64_t)c->sms * 8);
         switch (c->dim) {
         case 16: rb::table_keys_kernel<16><<<blocks, 256, 0, c->stream>>>(c->refs.as<float>(), n, c->dim, r0, rows, keys_in, vals_in); break;
@@ -1170,10 +1196,10 @@ int riann_model_build_tables(riann_ctx *c)
         }
         CK(cudaGetLastError());
         // index-ordered distances are the unsorted keys
-        CK(cudaMemcpyAsync(c->dmat.as<float>() + (size_t)r0 * n, keys_in, (size_t)rows * n * 4,
+        CK(cudaMemcpyAsync(c->dmat.as<float>() + ro, keys_in, (size_t)rows * n * 4,
                            cudaMemcpyDeviceToDevice, c->stream));
-        uint32_t *kout = reinterpret_cast<uint32_t *>(c->sdist.as<float>() + (size_t)r0 * n);
-        int32_t *vout = c->idx16 ? vals_out : c->sidx.as<int32_t>() + (size_t)r0 * n;
+        uint32_t *kout = reinterpret_cast<uint32_t *>(c->sdist.as<float>() + ro);
+        int32_t *vout = c->idx16 ? vals_out : c->sidx.as<int32_t>() + ro;
         CK(cub::DeviceSegmentedRadixSort::SortPairs(temp.p, temp_bytes, keys_in, kout, vals_in, vout,
                                                      (int)(rows * n), (int)rows, d_off.as<int>(),
                                                      d_off.as<int>() + 1, 0, 32, c->stream));
@@ -1181,7 +1207,7 @@ int riann_model_build_tables(riann_ctx *c)
         CK(cudaGetLastError());
         if (c->idx16) {
             rb::narrow_u16_kernel<<<(unsigned)((rows * n + 255) / 256), 256, 0, c->stream>>>(
-                vout, c->sidx.as<uint16_t>() + (size_t)r0 * n, rows * n);
+                vout, c->sidx.as<uint16_t>() + ro, rows * n);
             CK(cudaGetLastError());
         }
     }
@@ -1189,18 +1215,103 @@ int riann_model_build_tables(riann_ctx *c)
     temp.release();
     d_off.release();
     c->keys.release();
+    return 0;
+}
+
+int riann_model_build_tables(riann_ctx *c)
+{
+    RET(check_model(c, false));
+    RET(c->use());
+    RET(build_table_rows(c, 0, c->n));
     RET(build_bulk_tables(c));
+    c->nshards = 0;
+    c->own_row0 = 0;
+    c->own_rows = c->n;
     c->tables = true;
+    return 0;
+}
+
+int riann_model_build_table_rows(riann_ctx *c, int64_t row0, int64_t rows)
+{
+    RET(check_model(c, false));
+    if (row0 < 0 || rows < 1 || row0 + rows > c->n)
+        return fail(RIANN_E_INDEX, "rows [%lld, %lld) out of range for %lld references", (long long)row0,
+                    (long long)(row0 + rows), (long long)c->n);
+    RET(c->use());
+    c->pos.release();
+    c->coarse.release();
+    c->coarse1.release();
+    RET(build_table_rows(c, row0, rows));
+    c->nshards = 0;
+    c->own_row0 = row0;
+    c->own_rows = rows;
+    c->tables = row0 == 0 && rows == c->n;
+    if (c->tables) RET(build_bulk_tables(c));
+    return 0;
+}
+
+int riann_model_table_ptrs(riann_ctx *c, void **sd, void **si, void **dm, int64_t *row0, int64_t *rows)
+{
+    RET(check_model(c, false));
+    if (c->own_rows < 0 || !c->sdist.p) return fail(RIANN_E_STATE, "context holds no table rows");
+    if (sd) *sd = c->sdist.p;
+    if (si) *si = c->sidx.p;
+    if (dm) *dm = c->dmat.p;
+    if (row0) *row0 = c->own_row0;
+    if (rows) *rows = c->own_rows;
+    return 0;
+}
+
+int riann_model_attach_shards(riann_ctx *c, int nshards, int64_t shard_rows, void *const *sd, void *const *si,
+                              void *const *dm)
+{
+    RET(check_model(c, false));
+    if (nshards < 1 || nshards > 64 || shard_rows < 1 || (int64_t)nshards * shard_rows < c->n ||
+        (int64_t)(nshards - 1) * shard_rows >= c->n)
+        return fail(RIANN_E_VALUE, "%d shards of %lld rows do not tile %lld rows", nshards, (long long)shard_rows,
+                    (long long)c->n);
+    RET(c->use());
+    // peer access to shards on other GPUs (NVLink peer loads)
+    for (int s = 0; s < nshards; s++) {
+        for (void *ptr : {sd[s], si[s], dm[s]}) {
+            if (!ptr) return fail(RIANN_E_VALUE, "shard %d has a null table pointer", s);
+            cudaPointerAttributes at;
+            CK(cudaPointerGetAttributes(&at, ptr));
+            if (at.type != cudaMemoryTypeDevice) return fail(RIANN_E_VALUE, "shard %d is not device memory", s);
+            if (at.device != c->device) {
+                int ok = 0;
+                CK(cudaDeviceCanAccessPeer(&ok, c->device, at.device));
+                if (!ok) return fail(RIANN_E_UNSUPPORTED, "device %d cannot access peer %d", c->device, at.device);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                cudaGetLastError();
+            }
+        }
+    }
+    std::vector<const void *> ptrs;
+    for (int s = 0; s < nshards; s++) ptrs.push_back(sd[s]);
+    for (int s = 0; s < nshards; s++) ptrs.push_back(si[s]);
+    for (int s = 0; s < nshards; s++) ptrs.push_back(dm[s]);
+    RET(c->sh_ptrs.ensure(ptrs.size() * sizeof(void *)));
+    CK(cudaMemcpy(c->sh_ptrs.p, ptrs.data(), ptrs.size() * sizeof(void *), cudaMemcpyHostToDevice));
+    c->nshards = nshards;
+    c->shard_rows = shard_rows;
+    c->idx16 = c->n <= 65536;
+    c->tables = true;
+    c->field_count = -1;
     return 0;
 }
 
 int riann_model_get_tables(riann_ctx *c, int64_t row0, int64_t rows, float *sd, int32_t *si)
 {
-    RET(check_model(c, true));
-    if (row0 < 0 || rows < 0 || row0 + rows > c->n) return fail(RIANN_E_INDEX, "rows out of range");
+    RET(check_model(c, false));
+    if (c->nshards > 0) return fail(RIANN_E_UNSUPPORTED, "tables are attached shards: read them from their owners");
+    if (c->own_rows < 0) return fail(RIANN_E_STATE, "model has no sorted tables");
+    if (row0 < c->own_row0 || rows < 0 || row0 + rows > c->own_row0 + c->own_rows)
+        return fail(RIANN_E_INDEX, "rows out of range");
     RET(c->use());
     const int64_t n = c->n;
-    const size_t off = (size_t)row0 * n, cnt = (size_t)rows * n;
+    const size_t off = (size_t)(row0 - c->own_row0) * n, cnt = (size_t)rows * n;
     if (sd) CK(cudaMemcpyAsync(sd, c->sdist.as<float>() + off, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
     if (si) {
         if (!c->idx16) {
@@ -1647,6 +1758,7 @@ int riann_extract_patches(riann_ctx *c, const float *frame, int H, int W, int C,
 
 int riann_ring_candidates(riann_ctx *c, int64_t anchor, double d, double eps, int64_t *lo, int64_t *hi, int32_t *out)
 {
+    if (c && c->nshards > 0) return fail(RIANN_E_UNSUPPORTED, "ring_candidates on attached shards");
     RET(check_model(c, true));
     if (anchor < 0 || anchor >= c->n)
         return fail(RIANN_E_INDEX, "anchor %lld out of range for %lld references", (long long)anchor, (long long)c->n);

@@ -284,7 +284,48 @@ struct QueryParams {
     int passes;           // radix passes for indices < n
     const int32_t *qlist; // optional: process only these queries (count *n_qlist)
     const int32_t *n_qlist;
+    // row-sharded tables (config 4: n x n tables larger than one GPU): row a of
+    // each table lives in shard s = a / shard_rows at sh_*[s] + (a - s * shard_rows) * n,
+    // on this GPU or a peer (NVLink peer pointers); nshards == 0: sdist/sidx/dmat above
+    const float *const *sh_sdist;
+    const void *const *sh_sidx;
+    const float *const *sh_dmat;
+    int64_t shard_rows;
+    int nshards;
 };
+
+__device__ __forceinline__ int64_t shard_of(const QueryParams &P, int64_t a, int64_t &r)
+{
+    const int64_t s = a / P.shard_rows;
+    r = a - s * P.shard_rows;
+    return s;
+}
+__device__ __forceinline__ const float *sdist_row(const QueryParams &P, int64_t a)
+{
+    if (P.nshards == 0) return P.sdist + a * P.n;
+    int64_t r;
+    const int64_t s = shard_of(P, a, r);
+    return P.sh_sdist[s] + r * P.n;
+}
+__device__ __forceinline__ const float *dmat_row(const QueryParams &P, int64_t a)
+{
+    if (P.nshards == 0) return P.dmat + a * P.n;
+    int64_t r;
+    const int64_t s = shard_of(P, a, r);
+    return P.sh_dmat[s] + r * P.n;
+}
+// sorted index row a as (base, element offset) for idx_at<IdxT>
+__device__ __forceinline__ const void *sidx_base(const QueryParams &P, int64_t a, int64_t &off)
+{
+    if (P.nshards == 0) {
+        off = a * P.n;
+        return P.sidx;
+    }
+    int64_t r;
+    const int64_t s = shard_of(P, a, r);
+    off = r * P.n;
+    return P.sh_sidx[s];
+}
 
 enum { ERR_PREV_RANGE = 3, ERR_USED_OVERFLOW = 5 };
 constexpr int LIST_BYTES = 4096;                      // per list, per warp, in shared memory
@@ -566,13 +607,15 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
         const double d = exact_dist_all<D>(P.refs, p, q, dim, lane);
         long long exact_cnt = 1;
         int64_t lo, hi;
-        ring_window(P.sdist + (int64_t)p * n, n, __dsub_rn(d, __dmul_rn(P.alpha, d)),
+        ring_window(sdist_row(P, p), n, __dsub_rn(d, __dmul_rn(P.alpha, d)),
                     __dadd_rn(d, __dmul_rn(P.alpha, d)), lane, lo, hi);
         int cS = (int)(hi - lo);
         const int first = cS;
         bool p_in = false;
+        int64_t prow_off;
+        const void *prow = sidx_base(P, p, prow_off);
         for (int64_t k = lo + lane; k < hi; k += 32) {
-            const uint32_t j = idx_at<IdxT>(P.sidx, (int64_t)p * n + k);
+            const uint32_t j = idx_at<IdxT>(prow, prow_off + k);
             A.put((int)(k - lo), j);
             p_in |= (j == (uint32_t)p);
         }
@@ -647,7 +690,7 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                 exact_cnt++;
                 const double lv = __dsub_rn(da, __dmul_rn(P.alpha, da));
                 const double hv = __dadd_rn(da, __dmul_rn(P.alpha, da));
-                const float *drow = P.dmat + (int64_t)a * n;
+                const float *drow = dmat_row(P, a);
                 int nh = 0;
                 for (int base = 0; base < cS; base += 256) {
                     uint32_t j[8];

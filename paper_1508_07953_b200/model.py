@@ -144,6 +144,10 @@ def resident(ctx: N.Context, model) -> None:
     tok = ctx.model_token
     if tok is not None and tok() is model:
         return
+    sharded = getattr(model, "_sharded", None)
+    if sharded is not None:  # row-sharded tables (shards.py)
+        sharded.attach(ctx, model)
+        return
     refs = np.ascontiguousarray(model.refs, dtype=np.float32)
     n, dim = refs.shape
     pw, ph = int(model.patch_size[0]), int(model.patch_size[1])

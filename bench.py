@@ -304,6 +304,43 @@ def device_frames_run(N, ctx, frames, y0, t_first, ev_pairs=None):
     return stats
 
 
+def band_projection(R, N, model, cfg, frames, Wm, K, local, bands=(2, 4, 8)):
+    """Per-GPU share of an N-GPU run measured on this GPU: grid-row band 0 of
+    N (frame rows [0, gh/N + ph - 1)) through the same frames, device-resident,
+    CUDA events.  The model is replicated in a real N-GPU run, so the band's
+    ms/frame is the projected per-GPU frame time (only one GPU is available
+    here)."""
+    import torch
+
+    from paper_1508_07953_b200.bands import BandStream, band_rows, frame_band
+
+    gw, gh = cfg.grid
+    ph = cfg.patch[1]
+    ctx = N.context(local)
+    ext = torch.cuda.ExternalStream(ctx.stream)
+    out = {}
+    for nb in bands:
+        y0, y1 = band_rows(gh, nb, 0)
+        bs = BandStream(model, gw, gh, y0, y1, R.SearchParams(), device=local)
+        for k in range(Wm):
+            bs.step(frame_band(frames[k], y0, y1, ph))
+        dev = [torch.from_numpy(frame_band(frames[Wm + k], y0, y1, ph)).cuda() for k in range(K)]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ctx.lock:
+            ctx.select(bs.slot)
+            with torch.cuda.stream(ext):
+                e0.record()
+                device_frames_run(N, ctx, dev, y0, Wm + 1)
+                e1.record()
+        e1.synchronize()
+        bs.close()
+        ms = e0.elapsed_time(e1) / K
+        out[f"gpus{nb}"] = {"band_rows": y1 - y0, "ms_per_frame_per_gpu": ms,
+                            "projected_query_patches_per_s": cfg.queries / ms * 1e3}
+    return out
+
+
 def config_line(R, N, cfg_id, local):
     """Throughput of another BASELINE config on this GPU: every frame of the
     clip through the device-resident path (frames pre-uploaded), frame 1
@@ -665,6 +702,11 @@ def run_ours(a):
                              f"C port of search.py:83-151 (oracle/), table rows built lazily before timing "
                              f"(cold pass {t_cold:.1f}s)"}
 
+    # ---- projected per-GPU frame time at N = 2 / 4 / 8 (band 0 of N on this GPU)
+    projection = None
+    if rank == 0 and world == 1 and not a.no_configs:
+        projection = band_projection(R, N, model, cfg, full_frames, Wm, K, local)
+
     # ---- other BASELINE configs on this GPU (N=1)
     configs = None
     if rank == 0 and world == 1 and not a.no_configs:
@@ -741,6 +783,7 @@ def run_ours(a):
             "parity": parity,
             "comparator": comp,
             "configs": configs,
+            "multi_gpu_projection": projection,
             "e2e": {"value": e2e, "unit": "query patches/s", "ms_per_step": 1e3 * t_e2e / K,
                     "h2d_bytes_per_step": int(sum(h.numel() for h in host[:1]) * 4 * world),
                     "d2h_bytes_per_step": d2h,

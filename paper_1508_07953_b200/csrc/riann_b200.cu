@@ -428,6 +428,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.starts = c->b_starts.as<int32_t>();
     B.gdesc = c->b_gdesc.as<int4>();
     B.item_next = ctr + 3;
+    B.fdirect = QN < 8 * n ? rb::FDIRECT : 0;  // few queries per anchor (a row band)
     B.out_idx = Pq.out_idx;
     B.out_dist = Pq.out_dist;
     B.stats = Pq.stats;

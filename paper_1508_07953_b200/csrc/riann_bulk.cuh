@@ -71,6 +71,15 @@ constexpr int FCAP = RIANN_FCAP;  // query descriptors per filter stage
 #endif
 constexpr int FW2 = RIANN_FILTER_WARPS;  // warps per filter CTA
 constexpr int LCAP = RIANN_FILTER_LCAP;  // list entries per filter sub-chunk
+#ifndef RIANN_FDIRECT
+#define RIANN_FDIRECT 64
+#endif
+// (anchor, half) items with at most fdirect list groups (8 entries each) look
+// ranks up in global memory instead of staging the half row (n bytes): one
+// 32-byte sector per entry against n / (8 * groups) bytes of row per entry.
+// Enabled by the host when queries per anchor are few (row bands on many
+// GPUs: measured -0.5 ms/frame at 1/8 of config 3, +0.3 ms on the whole frame).
+constexpr int FDIRECT = RIANN_FDIRECT;
 constexpr int FSEG = 256;        // list entries per final-scan fill round (8 per lane)
 
 enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
@@ -128,6 +137,7 @@ struct BulkParams {
     int32_t *starts;         // exclusive scan of counts
     int4 *gdesc;             // per active query in anchor order: (g, s_off/128, lo | lenA8/8 << 17, hi | lenB8/8 << 17)
     int32_t *item_next;      // filter work-item counter
+    int fdirect;             // filter: direct rank lookups for items of <= fdirect list groups
     int32_t *out_idx;
     double *out_dist;
     unsigned long long *stats;
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
     int4 *descb = reinterpret_cast<int4 *>(smem_f + n);
     int *qg0 = reinterpret_cast<int *>(descb + 2 * FCAP);
     __shared__ uint64_t dbar[2], rbar;
-    __shared__ int s_it[2], s_cnt[2], s_start[2], s_q1, s_ng;
+    __shared__ int s_it[2], s_cnt[2], s_start[2], s_ng, s_direct;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint8_t *bcur = cur ? P.bits1 : P.bits0;
     uint8_t *bnxt = cur ? P.bits0 : P.bits1;
@@ -545,8 +555,13 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                     s_ng = run;
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     if (first_sub) {
-                        mbar_expect_tx(&rbar, (unsigned)n);
-                        tma_bulk_g2s(row, P.pos + (int64_t)a * n + (int64_t)h * jh, (unsigned)n, &rbar);
+                        // few list groups for this (anchor, half): look the ranks up in
+                        // global memory (L2) instead of staging the n-byte half row
+                        s_direct = (cnt <= FCAP && run <= P.fdirect) ? 1 : 0;
+                        if (!s_direct) {
+                            mbar_expect_tx(&rbar, (unsigned)n);
+                            tma_bulk_g2s(row, P.pos + (int64_t)a * n + (int64_t)h * jh, (unsigned)n, &rbar);
+                        }
                     }
                 }
                 __syncwarp();
@@ -596,11 +611,13 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                         if (nit >= 0) fetch_desc(db ^ 1, nstart, min(ncnt, FCAP));
                     }
                 }
-                if (first_sub) {
+                const bool direct = s_direct != 0;  // block-uniform, set with s_ng
+                if (first_sub && !direct) {
                     mbar_wait(&rbar, rpar);
                     rpar ^= 1;
                 }
                 const uint32_t hoff = (uint32_t)(h * jh), jmax = (uint32_t)(jh - 1);
+                const uint16_t *grow = P.pos + (int64_t)a * n + (int64_t)h * jh;
 #pragma unroll
                 for (int k = 0; k < NPRE; k++) {
                     if (k * FW2 * 32 >= NG) break;  // block-uniform
@@ -614,8 +631,13 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                         // all eight lookups issued unconditionally (padding / dead entries
                         // clamped into the half row), the alive bits mask the result
                         uint32_t rk[8];
+                        if (direct) {
 #pragma unroll
-                        for (int x = 0; x < 8; x++) rk[x] = row[min((uint32_t)e8[x] - hoff, jmax)];
+                            for (int x = 0; x < 8; x++) rk[x] = __ldg(grow + min((uint32_t)e8[x] - hoff, jmax));
+                        } else {
+#pragma unroll
+                            for (int x = 0; x < 8; x++) rk[x] = row[min((uint32_t)e8[x] - hoff, jmax)];
+                        }
 #pragma unroll
                         for (int x = 0; x < 8; x++)
                             keep |= (rk[x] - lo < wlen ? 1u : 0u) << x;  // lo <= r < hi

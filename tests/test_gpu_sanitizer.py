@@ -1,0 +1,55 @@
+"""compute-sanitizer over a small stream (config 0 shape, both frame paths,
+the exact comparator and the effects pass): memcheck (out-of-bounds / misaligned
+global and shared accesses) and racecheck (shared-memory hazards of the
+mbarrier / TMA pipelines and warp-synchronous code) must report no errors."""
+
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_1508_07953_b200 as R
+from paper_1508_07953_b200 import workloads as W
+cfg = W.CONFIGS[0]
+frames = W.clip(cfg, 3)
+refs = W.reference_set(cfg)
+model = R.ReferenceModel.from_refs(refs, cfg.patch)
+for path in (0, 1):
+    R.set_frame_path(path)
+    for _, f, s in R.stream_fields(model, frames):
+        pass
+R.set_frame_path(0)
+R.field_exact_oracle(frames[0][:24, :24], model)
+print("SANITIZED_RUN_OK")
+''' % REPO
+
+
+def _sanitizer():
+    return shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_compute_sanitizer_clean(tool, tmp_path):
+    cs = _sanitizer()
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    script = tmp_path / "run.py"
+    script.write_text(SCRIPT)
+    cmd = [cs, "--tool", tool, "--error-exitcode", "3", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    r = subprocess.run(cmd + [sys.executable, str(script)], capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    assert "SANITIZED_RUN_OK" in out, out[-3000:]
+    assert r.returncode == 0, out[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-3000:]

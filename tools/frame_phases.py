@@ -23,7 +23,13 @@ frames = list(W.iter_clip(cfg, T))
 refs = W.reference_set(cfg)
 model = R.ReferenceModel.from_refs(refs, cfg.patch, channels=cfg.channels)
 gw, gh = cfg.grid
-bs = BandStream(model, gw, gh, 0, gh)
+nb = int(os.environ.get("BANDS", "1"))  # time band 0 of nb (the per-GPU share of an nb-GPU run)
+y1 = gh // nb
+if nb > 1:
+    from paper_1508_07953_b200.bands import frame_band
+
+    frames = [frame_band(f, 0, y1, cfg.patch[1]) for f in frames]
+bs = BandStream(model, gw, gh, 0, y1)
 ctx = bs.ctx
 lib = N.lib()
 names = [lib.riann_phase_name(k).decode().split(":")[1] for k in range(NPH)]

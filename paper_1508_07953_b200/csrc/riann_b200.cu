@@ -227,8 +227,8 @@ struct riann_ctx {
     DevBuf x_B, x_nr, x_center, x_scal, x_A, x_nq, x_cand, x_lb, x_ncand, x_ub, x_fb, x_q, x_idx, x_dist;
     uint64_t x_checked = 0, x_fallback = 0;
     // bulk-path frame buffers
-    DevBuf b_state, b_pool, b_bits, b_kept, b_active[2], b_heavy, b_heavy2, b_counters, b_counts, b_starts, b_gdesc,
-        overflow2;
+    DevBuf b_state, b_pool, b_bits, b_kept, b_active[2], b_heavy, b_heavy2, b_heavy3, b_counters, b_counts, b_starts,
+        b_gdesc, overflow2;
     // frame path
     DevBuf frame, units[2], prev, fld_idx[2], fld_dist, tc, tc_sum, stats, err, overflow, keys, kw, koff;
     DevBuf q_rings, q_evals, q_cand, q_first, q_scanned, q_scanned_len, small;
@@ -367,6 +367,10 @@ int launch_query_i(riann_ctx *c, rb::QueryParams &P)
     }
 }
 
+// P0-heavy queries the per-query kernel takes on the second stream; more than
+// this (a stream's first frame) run further bulk passes instead
+constexpr int64_t K2CAP = 16384;
+
 template <int D>
 int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
 {
@@ -385,7 +389,8 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     RET(c->b_counters.ensure(256));
     RET(c->b_counts.ensure((size_t)(n + 1) * 4));
     RET(c->b_starts.ensure((size_t)(n + 1) * 4));
-    // [0..1] active counts, [2] P0 heavy, [3] item counter, [4..5] pool top, [6] ring heavy
+    // [0..1] active counts, [2] P0 heavy, [3] item counter, [4..5] pool top, [6] ring heavy,
+    // [7] P0 heavy count handed to the second stream
     int32_t *ctr = c->b_counters.as<int32_t>();
     CK(cudaMemsetAsync(ctr, 0, 256, c->stream));
 
@@ -451,65 +456,10 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         CK(cudaEventRecord(c->ev_proj, c->stream3));
         c->launches += 1;
     }
-    // P0a: d_prev, first-ring windows, list allocation (four queries per warp)
-    tmark(c, PH_P0A);
-    {
-        auto k = rb::bulk_p0a_kernel<D>;
-        int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, 0));
-        k<<<(unsigned)(c->sms * std::max(bps, 1)), 256, 0, c->stream>>>(B);
-        CK(cudaGetLastError());
-        c->launches += 1;
-    }
-    // queries P0 could not take (first ring > LIGHT_MAX, pool full) run the
-    // per-query kernel on the second stream while the ring phases proceed
-    CK(cudaEventRecord(c->ev_p0, c->stream));
-    CK(cudaStreamWaitEvent(c->stream2, c->ev_p0, 0));
-    {
-        rb::QueryParams H = Pq;
-        H.qlist = B.heavy;
-        H.n_qlist = B.n_heavy;
-        cudaStream_t main = c->stream;
-        c->stream = c->stream2;
-        DevBuf keep = c->overflow;
-        c->overflow = c->overflow2;
-        const int r = c->idx16 ? launch_query_i<uint16_t>(c, H) : launch_query_i<int32_t>(c, H);
-        c->overflow2 = c->overflow;
-        c->overflow = keep;
-        c->stream = main;
-        RET(r);
-        c->launches += 1;
-    }
-    // P0b: sorted fixed lists + alive bits (warp per query, bitmap in shared memory)
-    tmark(c, PH_P0B);
-    {
-        const int wpb = RIANN_P0_WPB;
-        const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
-        auto k = rb::bulk_p0_kernel<D>;
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, wpb * 32, smem));
-        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::min(std::max(bps, 1), 8), (QN + wpb - 1) / wpb);
-        B.active_out = c->b_active[0].as<int32_t>();
-        B.n_active_out = ctr + 0;
-        k<<<(unsigned)std::max<int64_t>(blocks, 1), wpb * 32, smem, c->stream>>>(B);
-        CK(cudaGetLastError());
-        c->launches += 1;
-    }
     auto dk = rb::bulk_draw_kernel<D>;
     int d_bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d_bps, dk, 256, 0));
     const unsigned d_grid = (unsigned)(c->sms * std::max(d_bps, 1));
-    // first anchors (search.py:119-133): the draw kernel seeds each key's generator
-    tmark(c, PH_DRAW);
-    CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));  // the draw counts anchors
-    dk<<<d_grid, 256, 0, c->stream>>>(B, 1);
-    CK(cudaGetLastError());
-    c->launches += 1;
-    CK(cudaEventRecord(c->ev_heavy, c->stream2));
-    B.heavy = c->b_heavy2.as<int32_t>();
-    B.n_heavy = ctr + 6;
-    // ring phases: group by anchor -> filter (anchor rows through shared memory) -> draw
     auto fk = rb::bulk_filter_kernel;
     const size_t fsmem = rb::filter_smem(n);
     CK(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
@@ -521,64 +471,176 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     int w_bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w_bps, wk, 256, 0));
     const unsigned w_grid = (unsigned)(c->sms * std::max(w_bps, 1));
-    const int phases = Pq.max_rings - 1;
-    for (int ph = 0; ph < phases; ph++) {
-        const int in = ph & 1, out = in ^ 1;
-        B.active_in = c->b_active[in].as<int32_t>();
-        B.n_active_in = ctr + in;
-        B.active_out = c->b_active[out].as<int32_t>();
-        B.n_active_out = ctr + out;
-        if (ph >= 15) {  // long ring caps: stop once no query is left
-            int32_t h = 0;
-            CK(cudaMemcpyAsync(&h, ctr + in, 4, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-            if (h == 0) break;
+    int32_t *ring_heavy = c->b_heavy2.as<int32_t>();  // > BULK_U used anchors: K2 from scratch, all passes
+
+    // One pass of the bulk path over the queries qin[0 .. nin) (all queries when
+    // qin is null): P0a allocates lists from an empty pool; queries that do not
+    // fit go to heavy_out (count at ctr[2]).
+    auto one_pass = [&](const int32_t *qin, int64_t nin, int32_t *heavy_out, bool first_pass) -> int {
+        B.qin = qin;
+        B.n_qin = nin;
+        B.heavy = heavy_out;
+        B.n_heavy = ctr + 2;
+        if (!first_pass) {
+            CK(cudaMemsetAsync(ctr, 0, 4 * 4, c->stream));   // active counts, heavy count, item counter
+            CK(cudaMemsetAsync(ctr + 4, 0, 8, c->stream));   // pool top
         }
-        CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
-        CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
-        tmark(c, PH_GROUP);
-        rb::anchor_scan_kernel<<<1, rb::SCAN_T, 0, c->stream>>>(B.counts, B.starts, (int)(n + 1));
-        CK(cudaGetLastError());
-        rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
-        CK(cudaGetLastError());
-        tmark(c, PH_WINDOW);
-        wk<<<w_grid, 256, 0, c->stream>>>(B);
-        CK(cudaGetLastError());
-        tmark(c, PH_FILTER);
-        fk<<<f_grid, rb::FW2 * 32, fsmem, c->stream>>>(B, ph & 1);
-        CK(cudaGetLastError());
+        // P0a: d_prev, first-ring windows, list allocation (four queries per warp)
+        tmark(c, PH_P0A);
+        {
+            auto k = rb::bulk_p0a_kernel<D>;
+            int bps = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, 0));
+            k<<<(unsigned)(c->sms * std::max(bps, 1)), 256, 0, c->stream>>>(B);
+            CK(cudaGetLastError());
+            c->launches += 1;
+        }
+        if (first_pass) {
+            // the first K2CAP queries P0 could not take (first ring > LIGHT_MAX, pool
+            // full) run the per-query kernel on the second stream while the ring
+            // phases proceed; more than that (the first frame of a stream: random
+            // prev, first rings of ~70 % of n) take further bulk passes
+            // its count is copied (ctr[7]): later passes reuse ctr[2]
+            CK(cudaMemcpyAsync(ctr + 7, ctr + 2, 4, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaEventRecord(c->ev_p0, c->stream));
+            CK(cudaStreamWaitEvent(c->stream2, c->ev_p0, 0));
+            rb::QueryParams H = Pq;
+            H.qlist = heavy_out;
+            H.n_qlist = ctr + 7;
+            H.qlist_cap = K2CAP;
+            cudaStream_t main = c->stream;
+            c->stream = c->stream2;
+            DevBuf keep = c->overflow;
+            c->overflow = c->overflow2;
+            const int r = c->idx16 ? launch_query_i<uint16_t>(c, H) : launch_query_i<int32_t>(c, H);
+            c->overflow2 = c->overflow;
+            c->overflow = keep;
+            c->stream = main;
+            RET(r);
+            c->launches += 1;
+        }
+        // P0b: sorted fixed lists + alive bits (warp per query, bitmap in shared memory)
+        tmark(c, PH_P0B);
+        {
+            const int wpb = RIANN_P0_WPB;
+            const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
+            auto k = rb::bulk_p0_kernel<D>;
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int bps = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, wpb * 32, smem));
+            int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::min(std::max(bps, 1), 8), (QN + wpb - 1) / wpb);
+            B.active_out = c->b_active[0].as<int32_t>();
+            B.n_active_out = ctr + 0;
+            k<<<(unsigned)std::max<int64_t>(blocks, 1), wpb * 32, smem, c->stream>>>(B);
+            CK(cudaGetLastError());
+            c->launches += 1;
+        }
+        // first anchors (search.py:119-133): the draw kernel seeds each key's generator
         tmark(c, PH_DRAW);
+        B.heavy = ring_heavy;
+        B.n_heavy = ctr + 6;
         CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));  // the draw counts anchors
-        dk<<<d_grid, 256, 0, c->stream>>>(B, ph & 1);
-        CK(cudaGetLastError());
-        c->launches += 5;
-    }
-    // final scan of the light queries (PCA-basis screening)
-    tmark(c, PH_FINAL);
-    {
-        CK(cudaStreamWaitEvent(c->stream, c->ev_proj, 0));
-        rb::ScreenParams SP;
-        SP.refs_pca16 = c->refs_pca16.as<__half>();
-        SP.e16p = c->e16p.as<float>();
-        SP.units_pca = c->units_pca.as<float>();
-        SP.dq = c->pca_dq + 1e-12f;
-        SP.slack = c->pca_dq + c->pca_e16max + 2e-12f;
-        SP.one_plus_eta = 1.0f + c->pca_eta * 1.001f;
-        SP.one_minus_eta = 1.0f - c->pca_eta * 1.001f;
-        auto k = rb::bulk_final_kernel<D>;
-        const size_t smem = 8 * rb::final_warp_bytes();
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, smem));
-        int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::max(bps, 1), (QN + 7) / 8);
-        k<<<(unsigned)std::max<int64_t>(blocks, 1), 256, smem, c->stream>>>(B, SP);
+        dk<<<d_grid, 256, 0, c->stream>>>(B, 1);
         CK(cudaGetLastError());
         c->launches += 1;
+        if (first_pass) CK(cudaEventRecord(c->ev_heavy, c->stream2));
+        // ring phases: group by anchor -> filter (anchor rows through shared memory) -> draw
+        const int phases = Pq.max_rings - 1;
+        for (int ph = 0; ph < phases; ph++) {
+            const int in = ph & 1, out = in ^ 1;
+            B.active_in = c->b_active[in].as<int32_t>();
+            B.n_active_in = ctr + in;
+            B.active_out = c->b_active[out].as<int32_t>();
+            B.n_active_out = ctr + out;
+            if (ph >= 15) {  // long ring caps: stop once no query is left
+                int32_t h = 0;
+                CK(cudaMemcpyAsync(&h, ctr + in, 4, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+                if (h == 0) break;
+            }
+            CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
+            CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
+            tmark(c, PH_GROUP);
+            rb::anchor_scan_kernel<<<1, rb::SCAN_T, 0, c->stream>>>(B.counts, B.starts, (int)(n + 1));
+            CK(cudaGetLastError());
+            rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);
+            CK(cudaGetLastError());
+            tmark(c, PH_WINDOW);
+            wk<<<w_grid, 256, 0, c->stream>>>(B);
+            CK(cudaGetLastError());
+            tmark(c, PH_FILTER);
+            fk<<<f_grid, rb::FW2 * 32, fsmem, c->stream>>>(B, ph & 1);
+            CK(cudaGetLastError());
+            tmark(c, PH_DRAW);
+            CK(cudaMemsetAsync(B.counts, 0, (size_t)(n + 1) * 4, c->stream));  // the draw counts anchors
+            dk<<<d_grid, 256, 0, c->stream>>>(B, ph & 1);
+            CK(cudaGetLastError());
+            c->launches += 5;
+        }
+        // final scan of the light queries (PCA-basis screening)
+        tmark(c, PH_FINAL);
+        {
+            CK(cudaStreamWaitEvent(c->stream, c->ev_proj, 0));
+            rb::ScreenParams SP;
+            SP.refs_pca16 = c->refs_pca16.as<__half>();
+            SP.e16p = c->e16p.as<float>();
+            SP.units_pca = c->units_pca.as<float>();
+            SP.dq = c->pca_dq + 1e-12f;
+            SP.slack = c->pca_dq + c->pca_e16max + 2e-12f;
+            SP.one_plus_eta = 1.0f + c->pca_eta * 1.001f;
+            SP.one_minus_eta = 1.0f - c->pca_eta * 1.001f;
+            auto k = rb::bulk_final_kernel<D>;
+            const size_t smem = 8 * rb::final_warp_bytes();
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int bps = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 256, smem));
+            int64_t blocks = std::min<int64_t>((int64_t)c->sms * std::max(bps, 1), (QN + 7) / 8);
+            k<<<(unsigned)std::max<int64_t>(blocks, 1), 256, smem, c->stream>>>(B, SP);
+            CK(cudaGetLastError());
+            c->launches += 1;
+        }
+        return 0;
+    };
+    RET(one_pass(nullptr, 0, c->b_heavy.as<int32_t>(), true));
+    // more P0-heavy queries than K2CAP: bulk passes over the rest, pool reset each time
+    {
+        int32_t nh = 0;
+        CK(cudaMemcpyAsync(&nh, ctr + 2, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (nh > K2CAP) {
+            // b_heavy[0 .. K2CAP) stays with the second stream's K2; later passes
+            // alternate between the two halves of b_heavy3
+            const int64_t rest = nh - K2CAP;
+            RET(c->b_heavy3.ensure((size_t)rest * 8));
+            int32_t *bufs[2] = {c->b_heavy3.as<int32_t>(), c->b_heavy3.as<int32_t>() + rest};
+            const int32_t *qin = c->b_heavy.as<int32_t>() + K2CAP;
+            int64_t nin = rest;
+            for (int pass = 0; nin > 0; pass++) {
+                int32_t *hout = bufs[pass & 1];
+                RET(one_pass(qin, nin, hout, false));
+                int32_t nout = 0;
+                CK(cudaMemcpyAsync(&nout, ctr + 2, 4, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+                if (nout == 0) break;
+                if (nout >= nin) {
+                    // no progress (first rings > LIGHT_MAX or alone larger than the pool): K2
+                    rb::QueryParams H = Pq;
+                    H.qlist = hout;
+                    H.n_qlist = ctr + 2;
+                    const int r = c->idx16 ? launch_query_i<uint16_t>(c, H) : launch_query_i<int32_t>(c, H);
+                    RET(r);
+                    c->launches += 1;
+                    break;
+                }
+                qin = hout;
+                nin = nout;
+            }
+        }
     }
     // ring-phase stragglers (> BULK_U used anchors in S): per-query kernel from
     // scratch on the main stream, then join the second stream
-    Pq.qlist = B.heavy;
-    Pq.n_qlist = B.n_heavy;
+    Pq.qlist = ring_heavy;
+    Pq.n_qlist = ctr + 6;
     tmark(c, PH_TAIL);
     CK(cudaStreamWaitEvent(c->stream, c->ev_heavy, 0));
     return 1;
@@ -970,7 +1032,7 @@ int riann_ctx_destroy(riann_ctx *c)
     cudaStreamSynchronize(c->stream);
     DevBuf *bufs[] = {&c->refs, &c->refs16, &c->err16, &c->dmat, &c->pos, &c->coarse, &c->coarse1, &c->b_state, &c->b_pool,
                       &c->b_active[0], &c->b_active[1], &c->b_heavy, &c->b_counters, &c->b_counts, &c->b_starts,
-                      &c->b_gdesc, &c->b_bits, &c->b_kept, &c->b_heavy2, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p, &c->sh_ptrs,
+                      &c->b_gdesc, &c->b_bits, &c->b_kept, &c->b_heavy2, &c->b_heavy3, &c->overflow2, &c->pca_T, &c->refs_pca16, &c->e16p, &c->sh_ptrs,
                       &c->units_pca, &c->e16max, &c->snap_idx, &c->snap_units, &c->sdist, &c->sidx, &c->frame, &c->units[0], &c->units[1], &c->prev,
                       &c->fld_idx[0], &c->fld_idx[1], &c->fld_dist, &c->tc, &c->tc_sum, &c->stats,
                       &c->err, &c->overflow, &c->keys, &c->kw, &c->koff, &c->q_rings, &c->q_evals,

@@ -82,7 +82,7 @@ constexpr int LCAP = RIANN_FILTER_LCAP;  // list entries per filter sub-chunk
 constexpr int FDIRECT = RIANN_FDIRECT;
 constexpr int FSEG = 256;        // list entries per final-scan fill round (8 per lane)
 
-enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2 };
+enum { ST_DONE = 0, ST_ACTIVE = 1, ST_HEAVY = 2, ST_FINISHED = 3 };
 
 // Per-query state.  The candidate list is fixed after P0: S is the set of
 // alive entries (bit set in bits[sel]) of the list at pool[s_off ..
@@ -137,6 +137,8 @@ struct BulkParams {
     int32_t *starts;         // exclusive scan of counts
     int4 *gdesc;             // per active query in anchor order: (g, s_off/128, lo | lenA8/8 << 17, hi | lenB8/8 << 17)
     int32_t *item_next;      // filter work-item counter
+    const int32_t *qin;      // P0a: process only these queries (n_qin of them) -- later passes
+    int64_t n_qin;
     int fdirect;             // filter: direct rank lookups for items of <= fdirect list groups
     int32_t *out_idx;
     double *out_dist;
@@ -800,12 +802,13 @@ __global__ void __launch_bounds__(256, RIANN_P0A_MINB) bulk_p0a_kernel(BulkParam
     const int lane = threadIdx.x & 31, gl = lane & 7, gb = lane & ~7;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t ib = gwarp * 4; ib < P.Q; ib += nwarps * 4) {
+    const int64_t nq = P.qin ? P.n_qin : P.Q;
+    for (int64_t ib = gwarp * 4; ib < nq; ib += nwarps * 4) {
         const int64_t gi = ib + (lane >> 3);
-        const int64_t g = gi < P.Q ? gi : 0;
+        const int64_t g = gi < nq ? (P.qin ? (int64_t)P.qin[gi] : gi) : 0;
         const int p = P.prev[g];
-        const bool ok = gi < P.Q && p >= 0 && p < P.n;
-        if (gi < P.Q && !ok && gl == 0) {
+        const bool ok = gi < nq && p >= 0 && p < P.n;
+        if (gi < nq && !ok && gl == 0) {
             atomicExch(P.err, ERR_PREV_RANGE);
             P.st[g].status = ST_HEAVY + 100;  // skipped everywhere
         }
@@ -1292,6 +1295,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
         if (lane == 0) {
             P.out_idx[g] = bi;
             P.out_dist[g] = bd;
+            P.st[g].status = ST_FINISHED;  // later passes (pool-sized query batches) skip it
         }
         acc_r += sr.rings;
         acc_e += sr.rings + nscan;

@@ -284,6 +284,7 @@ struct QueryParams {
     int passes;           // radix passes for indices < n
     const int32_t *qlist; // optional: process only these queries (count *n_qlist)
     const int32_t *n_qlist;
+    int64_t qlist_cap;    // > 0: at most this many entries of qlist
     // row-sharded tables (config 4: n x n tables larger than one GPU): row a of
     // each table lives in shard s = a / shard_rows at sh_*[s] + (a - s * shard_rows) * n,
     // on this GPU or a peer (NVLink peer pointers); nshards == 0: sdist/sidx/dmat above
@@ -591,7 +592,8 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
     const uint64_t pol_keep = pol_evict_last();
 
     unsigned long long acc_r = 0, acc_e = 0, acc_c = 0, acc_f = 0, acc_t = 0, acc_x = 0;
-    const int64_t qn = P.qlist ? (int64_t)*P.n_qlist : P.Q;
+    int64_t qn = P.qlist ? (int64_t)*P.n_qlist : P.Q;
+    if (P.qlist && P.qlist_cap > 0 && qn > P.qlist_cap) qn = P.qlist_cap;
 
     for (int64_t gi = gwarp; gi < qn; gi += nwarps) {
         const int64_t g = P.qlist ? (int64_t)P.qlist[gi] : gi;

@@ -1015,11 +1015,11 @@ __global__ void __launch_bounds__(256, RIANN_WIN_MINB) bulk_window_kernel(BulkPa
 // ---------------------------------------------------------------------------
 // F: final scan of S u {prev} for every light query (status DONE).
 //
-// Screening in the references' PCA basis: q' = T^T q (cuBLAS SGEMM, pedantic
+// Screening in the references' PCA basis: q' = T^T q (proj_kernel, fp32 FMA
 // fp32) and r' = fp16(T^T r) (per-row bound e16p[r]).  For T with
 // ||T^T T - I|| <= eta, the true distance d = ||q - r|| satisfies
 //   (||q' - r'|| - dq - e16p[r]) / (1 + eta) <= d <= (||q' - r'|| + dq + e16p[r]) / (1 - eta)
-// (dq bounds the SGEMM rounding error).  Partial sums of squares over the
+// (dq bounds the GEMM rounding error, any order).  Partial sums of squares over the
 // leading 16-component chunks are lower bounds of the full sum, so a candidate
 // is abandoned as soon as its partial lower bound exceeds the best upper bound
 // (initially the previous match's exact distance).  Survivors of all chunks

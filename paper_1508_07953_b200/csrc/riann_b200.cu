@@ -691,7 +691,7 @@ int check_err(riann_ctx *c)
     CK(cudaStreamSynchronize(c->stream));
     if (h == rb::ERR_PREV_RANGE) return fail(RIANN_E_INDEX, "prev_index out of range for %lld references", (long long)c->n);
     if (h == rb::ERR_USED_OVERFLOW)
-        return fail(RIANN_E_UNSUPPORTED, "more than 32 used anchors remained in the candidate set");
+        return fail(RIANN_E_UNSUPPORTED, "more than 128 used anchors remained in the candidate set");
     if (h) return fail(RIANN_E_CUDA, "kernel error %d", h);
     return 0;
 }

@@ -330,6 +330,10 @@ __device__ __forceinline__ const void *sidx_base(const QueryParams &P, int64_t a
 
 enum { ERR_PREV_RANGE = 3, ERR_USED_OVERFLOW = 5 };
 constexpr int LIST_BYTES = 4096;                      // per list, per warp, in shared memory
+#ifndef RIANN_K2_UMAX
+#define RIANN_K2_UMAX 128
+#endif
+constexpr int UMAX = RIANN_K2_UMAX;                             // used anchors tracked inside S (K2), in the scratch words
 constexpr int K2_SMEM_BYTES = 2 * LIST_BYTES + 1024;  // two lists + 256-word scratch
 
 // Candidate list: the first LIST_BYTES/sizeof(T) entries in shared memory,
@@ -628,16 +632,19 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
         long long tests = 0;
         if (cS >= P.L && P.max_rings > 1) {
             warp_radix_sort(A, B, cS, P.passes, hist, lane);
-            // used anchors still inside S (search.py:120-122), lane-distributed,
-            // with their positions in S
-            int nu = 0, u_val = -1, u_pos = 0;
+            // used anchors still inside S (search.py:120-122) with their positions
+            // in S: (uv[i], up[i]) for i < nu in the scratch words (free after the
+            // sort), up to UMAX of them
+            uint32_t *uv = hist, *up = hist + UMAX;
+            int nu = 0;
             if (p_in) {
                 nu = 1;
                 if (lane == 0) {
-                    u_val = p;
-                    u_pos = list_lower_bound(A, cS, (uint32_t)p);
+                    uv[0] = (uint32_t)p;
+                    up[0] = (uint32_t)list_lower_bound(A, cS, (uint32_t)p);
                 }
             }
+            __syncwarp();
             bool have_rng = false;
             Pcg64 rng;
             while (cS >= P.L && rings < P.max_rings) {
@@ -672,19 +679,23 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                 const int k = (int)pcg_integers(rng, (uint64_t)na);
                 int pos = k;
                 for (int it = 0; it <= nu; it++) {
-                    const int c = __popc(__ballot_sync(FULL, lane < nu && u_pos <= pos));
+                    int c = 0;
+                    for (int b = 0; b < nu; b += 32)
+                        c += __popc(__ballot_sync(FULL, b + lane < nu && (int)up[b + lane] <= pos));
                     if (k + c == pos) break;
                     pos = k + c;
                 }
                 const int a = (int)A.get(pos);
-                if (nu >= 32) {
+                if (nu >= UMAX) {
                     if (lane == 0) atomicExch(P.err, ERR_USED_OVERFLOW);
                     break;
                 }
-                if (lane == nu) {
-                    u_val = a;
-                    u_pos = pos;
+                __syncwarp();
+                if (lane == 0) {
+                    uv[nu] = (uint32_t)a;
+                    up[nu] = (uint32_t)pos;
                 }
+                __syncwarp();
                 nu++;
                 // search.py:131-135: ring around the anchor, intersect with S by
                 // lookups in the anchor's index-ordered distance row
@@ -724,29 +735,31 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                     B = t;
                 }
                 cS = nh;
-                // used anchors still in S, with their new positions
-                bool keep = false;
-                if (lane < nu) {
-                    const double dv = (double)ld_stream(drow + u_val, pol_stream);
-                    keep = lv <= dv && dv <= hv;
-                }
-                const unsigned kb = __ballot_sync(FULL, keep);
-                int nv = -1, np = 0;
-                int src = 0;
-                for (int i = 0; i < nu; i++) {
-                    const int vi = __shfl_sync(FULL, u_val, i);
-                    if ((kb >> i) & 1u) {
-                        if (lane == src) {
-                            nv = vi;
-                            np = list_lower_bound(A, cS, (uint32_t)vi);
-                        }
-                        src++;
+                // used anchors still in S (stable compaction), with their new positions
+                int nkeep = 0;
+                bool pin = false;
+                for (int b = 0; b < nu; b += 32) {
+                    const int i = b + lane;
+                    const uint32_t vi = i < nu ? uv[i] : 0u;
+                    bool keep = false;
+                    if (i < nu) {
+                        const double dv = (double)ld_stream(drow + vi, pol_stream);
+                        keep = lv <= dv && dv <= hv;
                     }
+                    const unsigned kb = __ballot_sync(FULL, keep);
+                    const int np = keep ? list_lower_bound(A, cS, vi) : 0;
+                    __syncwarp();
+                    if (keep) {
+                        const int o = nkeep + __popc(kb & lanemask_lt());
+                        uv[o] = vi;
+                        up[o] = (uint32_t)np;
+                        pin |= vi == (uint32_t)p;
+                    }
+                    nkeep += __popc(kb);
+                    __syncwarp();
                 }
-                nu = src;
-                u_val = nv;
-                u_pos = np;
-                p_in = __any_sync(FULL, lane < nu && u_val == p);
+                nu = nkeep;
+                p_in = __any_sync(FULL, pin);
             }
         } else if (cS > 0 && P.scanned) {
             // no rings drawn: order is irrelevant to the argmin, but the scanned

@@ -440,7 +440,7 @@ def test_model_switch_smaller_n(R, oracle_mod):
         prev = idx
 
 
-@pytest.mark.parametrize("L,alpha,max_rings", [(4, 0.3, 12), (1, 0.25, 2), (50, 0.1, 8)])
+@pytest.mark.parametrize("L,alpha,max_rings", [(4, 0.3, 12), (1, 0.25, 2), (50, 0.1, 8), (1, 0.9, 80)])
 def test_frame_path_search_params(R, oracle_mod, L, alpha, max_rings):
     """Non-default SearchParams through the bulk path: long ring caps (more
     used anchors than the draw kernel tracks: those queries are finished by K2
@@ -484,3 +484,31 @@ def test_frame_path_k2_only_model(R, oracle_mod):
         assert np.array_equal(_bits(fld.distances), _bits(dist)), t
         assert st.total_rings == ost["total_rings"] and st.total_distance_evals == ost["total_distance_evals"]
         prev = idx
+
+
+def test_many_used_anchors_inside_s(R, oracle_mod):
+    """A drawn anchor stays inside S only if its own ring contains it, i.e. at
+    distance 0 (search.py:131-135): 50 exact copies of the query among the
+    references, L = 1, max_rings = 80.  Every draw picks a copy and keeps S, so
+    the used anchors inside S (prev included) grow to 50 until avail is empty
+    (search.py:122-124).  K2 tracks up to 128 of them (was 32:
+    NotImplementedError).  All outputs equal the oracle's."""
+    rng = np.random.default_rng(8)
+    other, _ = R.normalize_rows(rng.normal(size=(250, 64)).astype(np.float32))
+    v = other[:1]
+    refs = np.concatenate([other[1:100], np.repeat(v, 50, axis=0), other[100:]])
+    model = R.ReferenceModel.from_refs(refs, (64, 1))
+    dup = np.arange(99, 149)
+    q = np.repeat(v, 8, axis=0)
+    prev = dup[rng.integers(0, 50, 8)]
+    params = R.SearchParams(L=1, alpha=0.25, max_rings=80)
+    keys = [(3, int(i), 1, 2) for i in range(8)]
+    res = R.riann_query_batch(model, q, prev, params, keys=keys, scanned=True)
+    sd, si = model.table_rows(0, model.n)
+    om = oracle_mod.OracleModel(refs, sd, si)
+    for i in range(8):
+        r = oracle_mod.query(om, q[i], int(prev[i]), L=1, alpha=0.25, max_rings=80, key=keys[i])
+        assert r["match_index"] == res["idx"][i] and r["rings_drawn"] == res["rings"][i], i
+        assert r["distance_evals"] == res["evals"][i] and r["candidates_final"] == res["cand"][i], i
+        assert np.array_equal(r["scanned"], res["scanned"][i]), i
+    assert (res["rings"] == 50).all()  # first ring + 49 draws: prev is a used copy too

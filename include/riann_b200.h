@@ -64,6 +64,8 @@ typedef struct {
 } riann_frame_stats;
 
 int riann_abi_version(void);
+/* 1 when the library was built with device-side bounds checks (-DRIANN_BOUNDS) */
+int riann_debug_checks(void);
 const char *riann_last_error(void);
 
 /* ---- context ---------------------------------------------------------- */

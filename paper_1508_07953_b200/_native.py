@@ -43,6 +43,7 @@ i32, i64, u32, u64, dbl = C.c_int, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 # name -> (restype, argtypes); every symbol include/riann_b200.h declares
 SIGNATURES = {
     "riann_abi_version": (i32, []),
+    "riann_debug_checks": (i32, []),
     "riann_last_error": (C.c_char_p, []),
     "riann_ctx_create": (i32, [i32, C.POINTER(P)]),
     "riann_ctx_destroy": (i32, [P]),

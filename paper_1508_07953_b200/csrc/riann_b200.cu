@@ -689,6 +689,17 @@ int check_err(riann_ctx *c)
     int h = 0;
     CK(cudaMemcpyAsync(&h, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+#ifdef RIANN_BOUNDS
+    {
+        CK(cudaDeviceSynchronize());
+        unsigned site = 0, zero = 0;
+        CK(cudaMemcpyFromSymbol(&site, rb::rb_bounds_site, 4));
+        if (site) {
+            CK(cudaMemcpyToSymbol(rb::rb_bounds_site, &zero, 4));
+            return fail(RIANN_E_CUDA, "device bounds check failed at site %u", site);
+        }
+    }
+#endif
     if (h == rb::ERR_PREV_RANGE) return fail(RIANN_E_INDEX, "prev_index out of range for %lld references", (long long)c->n);
     if (h == rb::ERR_USED_OVERFLOW)
         return fail(RIANN_E_UNSUPPORTED, "more than 128 used anchors remained in the candidate set");
@@ -989,6 +1000,14 @@ double h_pairwise(const double *a, int64_t n)
 extern "C" {
 
 int riann_abi_version(void) { return RIANN_ABI_VERSION; }
+int riann_debug_checks(void)
+{
+#ifdef RIANN_BOUNDS
+    return 1;
+#else
+    return 0;
+#endif
+}
 const char *riann_last_error(void) { return g_err.c_str(); }
 
 int riann_ctx_create(int device, riann_ctx **out)

@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
         const int lp = (wp >> 2) & 31;
         below = __shfl_sync(FULL, below, lp);
         p_in = __shfl_sync(FULL, p_in, lp);
+        RB_CHECK(run == cS && cA <= cS && lenA8 + lenB8 <= alloc && below <= cS, 10);
         // alive bits of the list (both buffers zero past the list end, whole words)
         {
             const int nb = (lenA8 + lenB8) >> 3, nbw = alloc >> 3;
@@ -363,6 +364,8 @@ __global__ void bulk_scatter_kernel(BulkParams P)
         const int g = P.active_in[i];
         const QState &s = P.st[g];
         const int a = s.anchor;
+        RB_CHECK(a >= 0 && a < P.n, 45);
+        RB_CHECK(P.starts[a] + P.counts[a] < m + 1, 46);
         P.gdesc[P.starts[a] + atomicAdd(P.counts + a, 1)] =
             make_int4(g, (int)(s.s_off >> 7), s.lo | ((s.lenA8 >> 3) << 17), s.hi | ((s.lenB8 >> 3) << 17));
     }
@@ -596,8 +599,10 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                             else r = mid;
                         }
                         const int4 d = desc[x];
+                        RB_CHECK(x < m && d.x >= 0 && d.x < P.Q, 20);
                         qi[k] = x;
                         eb[k] = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0) + (int64_t)(G - qg0[x]) * 8;
+                        RB_CHECK(eb[k] >= 0 && eb[k] + 8 <= P.pool_cap, 21);
                         al[k] = bcur[eb[k] >> 3];
                         v[k] = *reinterpret_cast<const uint4 *>(P.pool + eb[k]);
                     }
@@ -826,6 +831,8 @@ __global__ void __launch_bounds__(256, RIANN_P0A_MINB) bulk_p0a_kernel(BulkParam
                 off = (int64_t)atomicAdd(P.pool_top, (unsigned long long)alloc);
                 if (off + alloc > P.pool_cap) off = -1;
             }
+            RB_CHECK(lo >= 0 && lo <= hi && hi <= P.n, 1);
+            RB_CHECK(off < 0 || off + alloc <= P.pool_cap, 2);
             sp->d_prev = d;
             sp->lo = lo;
             sp->hi = hi;
@@ -950,7 +957,11 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
             if (!drew) apos = -1;
         }
         int an = 0;
-        if (drew && gl == 0) an = (int)P.pool[soff + apos];
+        if (drew && gl == 0) {
+            RB_CHECK(apos >= 0 && apos < W && soff + W <= P.pool_cap, 30);
+            an = (int)P.pool[soff + apos];
+            RB_CHECK(an >= 0 && an < P.n && nu < BULK_U, 31);
+        }
         an = __shfl_sync(FULL, an, gb);
         if (has && gl == 0) {
             sp->tests += cS;
@@ -1005,6 +1016,7 @@ __global__ void __launch_bounds__(256, RIANN_WIN_MINB) bulk_window_kernel(BulkPa
         int lo, hi;
         dist_window8<D>(P, a, qv, has, gl, gb, lo, hi);
         if (has && gl == 0) {
+            RB_CHECK(a >= 0 && a < P.n && lo >= 0 && lo <= hi && hi <= P.n, 40);
             d.z = (d.z & ~0x1ffff) | lo;
             d.w = (d.w & ~0x1ffff) | hi;
             P.gdesc[i] = d;
@@ -1165,6 +1177,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                 for (int x = 0; x < 8; x++)
                     if ((al >> x) & 1u) Cj[o++] = e8[x];
                 bn += __shfl_sync(FULL, inc, 31);
+                RB_CHECK(bn <= FB, 50);
                 lp += FSEG;
             }
             __syncwarp();
@@ -1291,6 +1304,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
         }
         flush();
         warp_argmin(bd, bi);
+        RB_CHECK(bi >= 0 && bi < P.n && sr.s_off + Wl <= P.pool_cap && sr.pin_pos < Wl, 51);
         const int nscan = cS + (p_in ? 0 : 1);
         if (lane == 0) {
             P.out_idx[g] = bi;

@@ -328,7 +328,23 @@ __device__ __forceinline__ const void *sidx_base(const QueryParams &P, int64_t a
     return P.sh_sidx[s];
 }
 
-enum { ERR_PREV_RANGE = 3, ERR_USED_OVERFLOW = 5 };
+enum { ERR_PREV_RANGE = 3, ERR_USED_OVERFLOW = 5, ERR_INTERNAL = 9 };
+
+// Bounds-checked builds (-DRIANN_BOUNDS, tests/test_gpu_bounds.py): index and
+// capacity invariants of the frame kernels checked on the device; the first
+// failing site is reported by riann_process_frame / riann_sync.  Stands in for
+// compute-sanitizer, which the GPU pool does not allow.
+#ifdef RIANN_BOUNDS
+__device__ unsigned rb_bounds_site;
+#define RB_CHECK(cond, site)                                                  \
+    do {                                                                      \
+        if (!(cond)) atomicCAS(&rb::rb_bounds_site, 0u, (unsigned)(site));    \
+    } while (0)
+#else
+#define RB_CHECK(cond, site) \
+    do {                     \
+    } while (0)
+#endif
 constexpr int LIST_BYTES = 4096;                      // per list, per warp, in shared memory
 #ifndef RIANN_K2_UMAX
 #define RIANN_K2_UMAX 128
@@ -616,6 +632,7 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
         ring_window(sdist_row(P, p), n, __dsub_rn(d, __dmul_rn(P.alpha, d)),
                     __dadd_rn(d, __dmul_rn(P.alpha, d)), lane, lo, hi);
         int cS = (int)(hi - lo);
+        RB_CHECK(lo >= 0 && lo <= hi && hi <= n, 60);
         const int first = cS;
         bool p_in = false;
         int64_t prow_off;
@@ -685,7 +702,9 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                     if (k + c == pos) break;
                     pos = k + c;
                 }
+                RB_CHECK(pos >= 0 && pos < cS, 61);
                 const int a = (int)A.get(pos);
+                RB_CHECK(a >= 0 && a < n, 62);
                 if (nu >= UMAX) {
                     if (lane == 0) atomicExch(P.err, ERR_USED_OVERFLOW);
                     break;

@@ -43,9 +43,9 @@ cfg = W.CONFIGS[0]
 clip = W.clip(cfg, 4)
 model = R.ReferenceModel.from_refs(W.reference_set(cfg), cfg.patch)
 for path in (0, 1):
-    R.set_frame_path(path)
+    N.set_frame_path(path)
     out["cfg0_path%%d" %% path] = digest([f for _, f, _ in R.stream_fields(model, clip)])
-R.set_frame_path(0)
+N.set_frame_path(0)
 q = R.frame_units(clip[1], model)[:500]
 res = R.riann_query_batch(model, q, np.arange(500) %% model.n, R.SearchParams(max_rings=20), keys=list(range(500)))
 out["batch"] = hashlib.sha256(res["idx"].tobytes() + res["dist"].tobytes()).hexdigest()

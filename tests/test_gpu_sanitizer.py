@@ -19,16 +19,17 @@ import sys
 sys.path.insert(0, %r)
 import numpy as np
 import paper_1508_07953_b200 as R
+from paper_1508_07953_b200 import _native as N
 from paper_1508_07953_b200 import workloads as W
 cfg = W.CONFIGS[0]
 frames = W.clip(cfg, 3)
 refs = W.reference_set(cfg)
 model = R.ReferenceModel.from_refs(refs, cfg.patch)
 for path in (0, 1):
-    R.set_frame_path(path)
+    N.set_frame_path(path)
     for _, f, s in R.stream_fields(model, frames):
         pass
-R.set_frame_path(0)
+N.set_frame_path(0)
 R.field_exact_oracle(frames[0][:24, :24], model)
 print("SANITIZED_RUN_OK")
 ''' % REPO

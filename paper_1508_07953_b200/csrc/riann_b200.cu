@@ -449,7 +449,12 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         const int64_t tiles = (QN + CF::PQ - 1) / CF::PQ;
         int bps = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, rb::proj_kernel<D>, CF::THREADS, 0));
-        const int64_t grid = std::min<int64_t>(tiles, (int64_t)c->sms * std::max(bps, 1));
+#ifndef RIANN_PROJ_PERSIST
+#define RIANN_PROJ_PERSIST 0
+#endif
+        // one tile per CTA (not persistent): with the side stream at low priority the
+        // block scheduler gives freed SM slots to the frame kernels first
+        const int64_t grid = RIANN_PROJ_PERSIST ? std::min<int64_t>(tiles, (int64_t)c->sms * std::max(bps, 1)) : tiles;
         rb::proj_kernel<D><<<(unsigned)std::max<int64_t>(grid, 1), CF::THREADS, 0, c->stream3>>>(
             Pq.units, c->pca_T.as<float>(), QN, c->units_pca.as<float>());
         CK(cudaGetLastError());
@@ -1024,11 +1029,19 @@ int riann_ctx_create(int device, riann_ctx **out)
     c->device = device;
     c->sms = prop.multiProcessorCount;
     c->smem_optin = (int)prop.sharedMemPerBlockOptin;
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
+    // stream priorities: the frame path first, the side streams (K2 stragglers,
+    // projection / temporal-change tree) fill idle SM slots
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+#ifndef RIANN_STREAM_PRIO
+#define RIANN_STREAM_PRIO 1
+#endif
+    if (!RIANN_STREAM_PRIO) prio_lo = prio_hi = 0;
+    cudaError_t e = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_lo);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p0, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_heavy, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->stream3, cudaStreamNonBlocking, prio_lo);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_units, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_proj, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_tc, cudaEventDisableTiming);

@@ -1413,10 +1413,16 @@ __global__ void __launch_bounds__(SCAN_T) anchor_scan_kernel(int32_t *counts, in
 // Each CTA owns PQ queries x all D outputs; K staged through shared memory in
 // chunks of PK.  Any summation order keeps the screening bound dq
 // (gamma_D * sqrt(D) * ||q||, build_pca) valid.
+#ifndef RIANN_PROJ_PQ
+#define RIANN_PROJ_PQ 64
+#endif
+#ifndef RIANN_PROJ_TM
+#define RIANN_PROJ_TM 8
+#endif
 template <int D>
 struct ProjCfg {
-    static constexpr int PQ = 64;               // queries per CTA
-    static constexpr int TM = 8;                // queries per thread
+    static constexpr int PQ = RIANN_PROJ_PQ;    // queries per CTA
+    static constexpr int TM = RIANN_PROJ_TM;    // queries per thread
     static constexpr int TN = D == 192 ? 12 : 4;  // outputs per thread
     static constexpr int THREADS = (PQ / TM) * (D / TN);
     static constexpr int PK = 32;               // k per stage

@@ -670,7 +670,8 @@ def run_ours(a):
     qpath_ms = allmax(ms3[1] / K)
     evals = allsum(sum(s.total_distance_evals for s in fstats)) / allsum(sum(s.queries for s in fstats))
     names = phase_names(N)
-    phase_ms = {names[k].split(":")[1]: allmax(phases[k] / K) for k in range(NPH) if phases[k] > 0}
+    phase_all = [allmax(phases[k] / K) for k in range(NPH)]  # every rank joins every collective
+    phase_ms = {names[k].split(":")[1]: phase_all[k] for k in range(NPH) if phase_all[k] > 0}
 
     # ---- CPU baseline: oracle on a sample of the last frame (rank 0, N=1)
     cpu = None

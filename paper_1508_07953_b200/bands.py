@@ -259,6 +259,8 @@ class DistributedStream:
         self.host = (torch.empty((self.world, 5 * self.m), dtype=torch.int32, pin_memory=True)
                      if self.rank == 0 else None)
         self.counters = torch.zeros(6, dtype=torch.int64, device=self.dev)
+        # the buffers were filled on torch's stream; the library stream is non-blocking
+        torch.cuda.synchronize(self.dev)
         self.t = 0
         self.cur = 0
 

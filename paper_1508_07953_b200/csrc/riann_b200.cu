@@ -656,6 +656,7 @@ int launch_query(riann_ctx *c, rb::QueryParams &P)
     P.refs16 = c->refs16.as<__half>();
     P.err16 = c->err16.as<float>();
     P.dmat = c->dmat.as<float>();
+    P.pos = (c->nshards == 0 && c->idx16 && c->pos.p) ? c->pos.as<uint16_t>() : nullptr;
     if (c->nshards > 0) {
         // row-sharded tables: the per-query kernel reads rows through the shard table
         const void *const *sp = c->sh_ptrs.as<const void *const>();
@@ -873,7 +874,16 @@ int launch_units(riann_ctx *c, const float *frame, int H, int W, int C, float *u
     U.tc = tc;
     if (U.Q <= 0) return 0;
     unsigned blocks = (unsigned)((U.Q + 127) / 128);
-    if (c->pw == 8 && c->ph == 8 && c->dim == 64) {
+#ifndef RIANN_K1_TILE
+#define RIANN_K1_TILE 1
+#endif
+    const int64_t k1_tiles = (int64_t)((U.gw + rb::K1_TW - 1) / rb::K1_TW) * ((H - c->ph + 1 + rb::K1_TH - 1) / rb::K1_TH);
+    const unsigned k1_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k1_tiles, (int64_t)c->sms * 8));
+    if (RIANN_K1_TILE && c->pw == 8 && c->ph == 8 && c->dim == 64 && C == 1) {
+        rb::units_tile_kernel<64><<<k1_grid, 256, 0, c->stream>>>(U);
+    } else if (RIANN_K1_TILE && c->pw == 8 && c->ph == 8 && c->dim == 192 && C == 3) {
+        rb::units_tile_kernel<192><<<k1_grid, 256, 0, c->stream>>>(U);
+    } else if (c->pw == 8 && c->ph == 8 && c->dim == 64) {
         const unsigned b = (unsigned)std::min<int64_t>((U.Q + 31) / 32, (int64_t)c->sms * 16);
         rb::units_warp_kernel<64><<<b, 256, 0, c->stream>>>(U);
     } else if (c->pw == 8 && c->ph == 8 && c->dim == 192) {
@@ -1213,7 +1223,9 @@ int riann_model_set_tables(riann_ctx *c, const float *sd, const int32_t *si)
     c->idx16 = n <= 65536;
     RET(c->sdist.ensure(cnt * 4));
     RET(c->sidx.ensure(cnt * (c->idx16 ? 2 : 4)));
-    RET(c->dmat.ensure(cnt * 4));
+    // index-ordered distance rows only for n > 65,536 (rank rows serve K2 otherwise)
+    if (c->idx16) c->dmat.release();
+    else RET(c->dmat.ensure(cnt * 4));
     CK(cudaMemcpyAsync(c->sdist.p, sd, cnt * 4, cudaMemcpyHostToDevice, c->stream));
     // index rows in chunks through a staging buffer (narrowed to u16 when possible)
     const int64_t chunk_rows = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)n * 4)));
@@ -1227,8 +1239,6 @@ int riann_model_set_tables(riann_ctx *c, const float *sd, const int32_t *si)
         if (c->idx16) {
             uint16_t *dst = c->sidx.as<uint16_t>() + (size_t)r0 * n;
             rb::narrow_u16_kernel<<<blocks, 256, 0, c->stream>>>(stage.as<int32_t>(), dst, (int64_t)m);
-            rb::dmat_scatter_kernel<uint16_t><<<blocks, 256, 0, c->stream>>>(
-                c->sdist.as<float>() + (size_t)r0 * n, dst, n, rows, c->dmat.as<float>() + (size_t)r0 * n);
         } else {
             int32_t *dst = c->sidx.as<int32_t>() + (size_t)r0 * n;
             CK(cudaMemcpyAsync(dst, stage.p, m * 4, cudaMemcpyDeviceToDevice, c->stream));
@@ -1249,14 +1259,17 @@ int riann_model_set_tables(riann_ctx *c, const float *sd, const int32_t *si)
 
 // K3 for table rows [row_lo, row_lo + nrows): sorted rows, index rows and the
 // index-ordered distance rows, stored from row_lo on (a shard holds a row range)
-int build_table_rows(riann_ctx *c, int64_t row_lo, int64_t nrows)
+int build_table_rows(riann_ctx *c, int64_t row_lo, int64_t nrows, bool want_dmat)
 {
     const int64_t n = c->n;
     const size_t tcnt = (size_t)nrows * n;
     c->idx16 = n <= 65536;
     RET(c->sdist.ensure(tcnt * 4));
     RET(c->sidx.ensure(tcnt * (c->idx16 ? 2 : 4)));
-    RET(c->dmat.ensure(tcnt * 4));
+    // index-ordered distance rows: only where the per-query kernel has no rank
+    // rows to use instead (row shards, n > 65,536)
+    if (want_dmat) RET(c->dmat.ensure(tcnt * 4));
+    else c->dmat.release();
     // row batches bounded by ~1 GiB of unsorted keys+values
     int64_t rb_rows = (int64_t)((1ull << 30) / ((size_t)n * 8));
     if (rb_rows < 1) rb_rows = 1;
@@ -1291,8 +1304,9 @@ int build_table_rows(riann_ctx *c, int64_t row_lo, int64_t nrows)
         }
         CK(cudaGetLastError());
         // index-ordered distances are the unsorted keys
-        CK(cudaMemcpyAsync(c->dmat.as<float>() + ro, keys_in, (size_t)rows * n * 4,
-                           cudaMemcpyDeviceToDevice, c->stream));
+        if (want_dmat)
+            CK(cudaMemcpyAsync(c->dmat.as<float>() + ro, keys_in, (size_t)rows * n * 4,
+                               cudaMemcpyDeviceToDevice, c->stream));
         uint32_t *kout = reinterpret_cast<uint32_t *>(c->sdist.as<float>() + ro);
         int32_t *vout = c->idx16 ? vals_out : c->sidx.as<int32_t>() + ro;
         CK(cub::DeviceSegmentedRadixSort::SortPairs(temp.p, temp_bytes, keys_in, kout, vals_in, vout,
@@ -1317,7 +1331,7 @@ int riann_model_build_tables(riann_ctx *c)
 {
     RET(check_model(c, false));
     RET(c->use());
-    RET(build_table_rows(c, 0, c->n));
+    RET(build_table_rows(c, 0, c->n, c->n > 65536));
     RET(build_bulk_tables(c));
     c->nshards = 0;
     c->own_row0 = 0;
@@ -1336,7 +1350,7 @@ int riann_model_build_table_rows(riann_ctx *c, int64_t row0, int64_t rows)
     c->pos.release();
     c->coarse.release();
     c->coarse1.release();
-    RET(build_table_rows(c, row0, rows));
+    RET(build_table_rows(c, row0, rows, true));  // shards: K2 reads dmat rows
     c->nshards = 0;
     c->own_row0 = row0;
     c->own_rows = rows;

@@ -134,6 +134,101 @@ __global__ void __launch_bounds__(256) units_warp_kernel(UnitsParams P)
     }
 }
 
+// K1 with the frame staged through shared memory: a CTA owns a tile of
+// K1_TW x K1_TH grid positions; the (K1_TH + 7) x (K1_TW + 7) x C frame region
+// it needs is loaded once, coalesced (float4 when the region is 16-byte
+// aligned), then every group of Lay<D>::G lanes builds its position's row from
+// shared memory with the same per-lane numpy accumulators as units_warp_kernel.
+constexpr int K1_TW = 32, K1_TH = 4;
+template <int D>
+__global__ void __launch_bounds__(256) units_tile_kernel(UnitsParams P)
+{
+    constexpr int G = Lay<D>::G, PER = Lay<D>::PER, NGB = 256 / G;  // groups per CTA
+    constexpr int C = D / 64;
+    constexpr int RW = K1_TW + 7, RH = K1_TH + 7;
+    constexpr int RF = RW * C;  // floats per region row
+    __shared__ __align__(16) float reg[RH * RF + 4];
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const int grp = threadIdx.x / G;
+    const int base = Lay<D>::base(gl);
+    const int gh = P.H - 7;
+    const int tiles_x = (P.gw + K1_TW - 1) / K1_TW, tiles_y = (gh + K1_TH - 1) / K1_TH;
+    const int64_t ntiles = (int64_t)tiles_x * tiles_y;
+    const int64_t WC = (int64_t)P.W * C;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int x0 = (int)(tile % tiles_x) * K1_TW, y0 = (int)(tile / tiles_x) * K1_TH;
+        __syncthreads();
+        const int cols = min(RW, P.W - x0) * C, rows = min(RH, P.H - y0);
+        const float *src = P.frame + (int64_t)y0 * WC + (int64_t)x0 * C;
+        if (((uintptr_t)src & 15) == 0 && (WC & 3) == 0) {
+            const int c4 = cols >> 2;
+            for (int e = threadIdx.x; e < rows * c4; e += 256) {
+                const int r = e / c4, k = e - r * c4;
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)r * WC) + k);
+                float *d = reg + r * RF + 4 * k;
+                d[0] = v.x;
+                d[1] = v.y;
+                d[2] = v.z;
+                d[3] = v.w;
+            }
+            for (int e = threadIdx.x; e < rows * (cols & 3); e += 256) {
+                const int r = e / (cols & 3), k = (c4 << 2) + e % (cols & 3);
+                reg[r * RF + k] = __ldg(src + (int64_t)r * WC + k);
+            }
+        } else {
+            for (int e = threadIdx.x; e < rows * cols; e += 256) {
+                const int r = e / cols, k = e - r * cols;
+                reg[r * RF + k] = __ldg(src + (int64_t)r * WC + k);
+            }
+        }
+        __syncthreads();
+        for (int pi = grp; pi < K1_TW * K1_TH; pi += NGB) {
+            const int tx = pi % K1_TW, ty = pi / K1_TW;
+            const int x = x0 + tx, y = y0 + ty;
+            const bool valid = x < P.gw && y < gh;
+            const int64_t g = valid ? (int64_t)y * P.gw + x : 0;
+            float v[PER];
+#pragma unroll
+            for (int i = 0; i < PER; i++) {
+                const int e = base + 8 * i;
+                const int c = e >> 6, dy = (e >> 3) & 7, dx = e & 7;
+                v[i] = valid ? reg[(ty + dy) * RF + (tx + dx) * C + c] : 0.f;
+            }
+            double acc = __dmul_rn((double)v[0], (double)v[0]);
+#pragma unroll
+            for (int i = 1; i < PER; i++) acc = __dadd_rn(acc, __dmul_rn((double)v[i], (double)v[i]));
+            acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 1));
+            acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 2));
+            acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 4));
+            if (G == 16) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, 8));
+            const double nr = __dsqrt_rn(acc);
+            const bool ok = nr >= 1e-12;
+            if (valid && P.norms && gl == 0) P.norms[g] = ok ? nr : 0.0;
+            if (!P.unit) continue;
+            float u[PER];
+#pragma unroll
+            for (int i = 0; i < PER; i++) u[i] = ok ? __double2float_rn(__ddiv_rn((double)v[i], nr)) : 0.0f;
+            if (valid) {
+                float *ur = P.unit + g * D + base;
+#pragma unroll
+                for (int i = 0; i < PER; i++) ur[8 * i] = u[i];
+            }
+            if (P.tc) {
+                const float *pr = P.prev_unit + g * D + base;
+                double t = sqdiff(u[0], __ldg(pr));
+#pragma unroll
+                for (int i = 1; i < PER; i++) t = __dadd_rn(t, sqdiff(u[i], __ldg(pr + 8 * i)));
+                t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 1));
+                t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 2));
+                t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 4));
+                if (G == 16) t = __dadd_rn(t, __shfl_xor_sync(FULL, t, 8));
+                if (valid && gl == 0) P.tc[g] = __dsqrt_rn(t);
+            }
+        }
+    }
+}
+
 // normalize_rows on explicit rows (patches.py:100-115); T = float or double
 // input (the reference converts any input to float64 first).
 template <class T>
@@ -293,6 +388,10 @@ struct QueryParams {
     const float *const *sh_dmat;
     int64_t shard_rows;
     int nshards;
+    // n <= 65,536 without shards: rank rows pos[a][j] (u16) replace the
+    // index-ordered distance rows; membership of j in a's ring is then
+    // lo_a <= pos[a][j] < hi_a with [lo_a, hi_a) the window on a's sorted row
+    const uint16_t *pos;
 };
 
 __device__ __forceinline__ int64_t shard_of(const QueryParams &P, int64_t a, int64_t &r)
@@ -722,7 +821,23 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                 exact_cnt++;
                 const double lv = __dsub_rn(da, __dmul_rn(P.alpha, da));
                 const double hv = __dadd_rn(da, __dmul_rn(P.alpha, da));
-                const float *drow = dmat_row(P, a);
+                // ring membership: rank in a's window (rank rows) or the value in
+                // a's index-ordered distance row -- the same searchsorted test
+                const bool use_pos = P.pos != nullptr;
+                const float *drow = use_pos ? nullptr : dmat_row(P, a);
+                const uint16_t *prank = use_pos ? P.pos + (int64_t)a * n : nullptr;
+                uint32_t a_lo = 0, a_w = 0;
+                if (use_pos) {
+                    int64_t wlo, whi;
+                    ring_window(sdist_row(P, a), n, lv, hv, lane, wlo, whi);
+                    a_lo = (uint32_t)wlo;
+                    a_w = (uint32_t)(whi - wlo);
+                }
+                auto member = [&](uint32_t jj, float dvf) {
+                    if (use_pos) return (uint32_t)__ldg(prank + jj) - a_lo < a_w;
+                    const double dv = (double)dvf;
+                    return lv <= dv && dv <= hv;
+                };
                 int nh = 0;
                 for (int base = 0; base < cS; base += 256) {
                     uint32_t j[8];
@@ -732,12 +847,13 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                         const int i = base + u * 32 + lane;
                         j[u] = i < cS ? A.get(i) : 0xffffffffu;
                     }
+                    if (!use_pos) {
 #pragma unroll
-                    for (int u = 0; u < 8; u++) v[u] = j[u] != 0xffffffffu ? ld_stream(drow + j[u], pol_stream) : 0.f;
+                        for (int u = 0; u < 8; u++) v[u] = j[u] != 0xffffffffu ? ld_stream(drow + j[u], pol_stream) : 0.f;
+                    }
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
-                        const double dv = (double)v[u];
-                        const bool keep = j[u] != 0xffffffffu && lv <= dv && dv <= hv;
+                        const bool keep = j[u] != 0xffffffffu && member(j[u], v[u]);
                         const unsigned ball = __ballot_sync(FULL, keep);
                         if (keep) B.put(nh + __popc(ball & lanemask_lt()), j[u]);
                         nh += __popc(ball);
@@ -761,10 +877,7 @@ __global__ void __launch_bounds__(256, 3) query_kernel(QueryParams P)
                     const int i = b + lane;
                     const uint32_t vi = i < nu ? uv[i] : 0u;
                     bool keep = false;
-                    if (i < nu) {
-                        const double dv = (double)ld_stream(drow + vi, pol_stream);
-                        keep = lv <= dv && dv <= hv;
-                    }
+                    if (i < nu) keep = member(vi, use_pos ? 0.f : ld_stream(drow + vi, pol_stream));
                     const unsigned kb = __ballot_sync(FULL, keep);
                     const int np = keep ? list_lower_bound(A, cS, vi) : 0;
                     __syncwarp();

@@ -377,7 +377,21 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     const int64_t QN = Pq.Q, n = c->n;
     RET(c->b_state.ensure((size_t)QN * sizeof(rb::QState)));
     // candidate pool: sum of first-ring sizes, capped (overflowing queries fall back to K2)
-    const size_t pool_entries = std::min<size_t>((size_t)QN * 8192, (size_t)6 << 30);
+    // candidate pool (u16 entries + two alive-bit buffers, 2.25 B per entry): up
+    // to 8,192 entries per query and 16 G entries, within 40 % of the free HBM
+    // (with what the pool already holds); a first frame whose first rings do
+    // not fit takes further passes
+    size_t pool_entries = std::min<size_t>((size_t)QN * 8192, (size_t)16 << 30);
+    if (pool_entries * 2 > c->b_pool.cap) {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        const size_t budget = (size_t)((double)(fr + c->b_pool.cap + c->b_bits.cap) * 0.4 / 2.25);
+        pool_entries = std::max<size_t>(std::min(pool_entries, budget), std::min<size_t>(pool_entries, (size_t)1 << 24));
+        pool_entries = std::max<size_t>(pool_entries, c->b_pool.cap / 2);
+    } else {
+        pool_entries = c->b_pool.cap / 2;
+    }
+    pool_entries &= ~(size_t)127;
     RET(c->b_pool.ensure(pool_entries * 2));
     RET(c->b_bits.ensure(pool_entries / 4));  // two alive-bit buffers
     RET(c->b_kept.ensure((size_t)QN * 4));

@@ -126,6 +126,9 @@ int riann_model_table_ptrs(riann_ctx *ctx, void **sdist, void **sidx, void **dma
  * rows).  The owners must outlive this context's use of the shards. */
 int riann_model_attach_shards(riann_ctx *ctx, int nshards, int64_t shard_rows, void *const *sdist,
                               void *const *sidx, void *const *dmat);
+/* Forget attached shards (before their owners free them): the context has no
+ * tables afterwards, so frame calls fail with RIANN_E_STATE. */
+int riann_model_detach_shards(riann_ctx *ctx);
 /* Download rows [row0, row0+rows) of the sorted tables. */
 int riann_model_get_tables(riann_ctx *ctx, int64_t row0, int64_t rows,
                            float *sorted_dist, int32_t *sorted_idx);

@@ -61,6 +61,7 @@ SIGNATURES = {
     "riann_model_build_table_rows": (i32, [P, i64, i64]),
     "riann_model_table_ptrs": (i32, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(i64), C.POINTER(i64)]),
     "riann_model_attach_shards": (i32, [P, i32, i64, P, P, P]),
+    "riann_model_detach_shards": (i32, [P]),
     "riann_process_frame": (i32, [P, P, i32, i32, i32, i32, P, u64, u32, i32, dbl, i32, C.c_uint,
                                   P, P, C.POINTER(FrameStatsC)]),
     "riann_set_prev_units": (i32, [P, P, i64, i32]),

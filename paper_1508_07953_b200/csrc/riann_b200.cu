@@ -1385,6 +1385,20 @@ int riann_model_table_ptrs(riann_ctx *c, void **sd, void **si, void **dm, int64_
     return 0;
 }
 
+int riann_model_detach_shards(riann_ctx *c)
+{
+    if (!c) return fail(RIANN_E_STATE, "null context");
+    RET(c->use());
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->nshards > 0) {
+        c->nshards = 0;
+        c->tables = false;
+        c->field_count = -1;
+        c->sh_ptrs.release();
+    }
+    return 0;
+}
+
 int riann_model_attach_shards(riann_ctx *c, int nshards, int64_t shard_rows, void *const *sd, void *const *si,
                               void *const *dm)
 {

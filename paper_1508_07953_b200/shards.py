@@ -67,6 +67,7 @@ class ShardedTables:
             si.append(b.value)
             dm.append(c.value)
         self._ptrs = tuple((C.c_void_p * S)(*v) for v in (sd, si, dm))
+        self._attached = []  # contexts holding these shards' pointers
 
     def table_rows(self, row0: int, rows: int):
         """Rows [row0, row0+rows) of one shard as (float32, int32), from its GPU."""
@@ -97,8 +98,20 @@ class ShardedTables:
             ctx.refs_token = ctx.model_token
             ctx.model_epoch += 1
             ctx.shards = self  # keep the owners alive while attached
+            if ctx not in self._attached:
+                self._attached.append(ctx)
 
     def close(self):
+        """Detach from every context still using the shards, then free them."""
+        for ctx in self._attached:
+            if getattr(ctx, "shards", None) is self and ctx.h:
+                with ctx.lock:
+                    N.check(N.lib().riann_model_detach_shards(ctx.h))
+                    ctx.model_token = None
+                    ctx.refs_token = None
+                    ctx.model_epoch += 1
+                    ctx.shards = None
+        self._attached = []
         for ctx in self.owners:
             ctx.close()
         self.owners = []

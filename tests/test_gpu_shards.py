@@ -87,3 +87,21 @@ def test_sharded_query_batch(R, oracle_mod):
         r = oracle_mod.query(om, q[i], int(prev[i]), key=keys[i])
         assert r["match_index"] == a["idx"][i] and r["rings_drawn"] == a["rings"][i]
     st.close()
+
+
+def test_closed_shards_fail_loudly(R):
+    """After ShardedTables.close() the querying context has no tables: a
+    later call re-attaches (model.resident) or fails, never reads freed rows."""
+    cfg, clip, refs, full, sharded, st = _setup(R, 1024, 2)
+    list(R.stream_fields(sharded, clip[:1]))
+    st.close()
+    object.__setattr__(sharded, "_sharded", None)
+    from paper_1508_07953_b200 import _native as N
+
+    ctx = N.context()
+    with ctx.lock:
+        assert ctx.model_token is None
+    # the model is simply re-made resident with its own tables
+    a = [f.indices.copy() for _, f, _ in R.stream_fields(sharded, clip)]
+    b = [f.indices.copy() for _, f, _ in R.stream_fields(full, clip)]
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))

@@ -161,6 +161,8 @@ int riann_timing_read(riann_ctx *ctx, double *ms3, uint64_t *frames, uint64_t *l
  * phases are NVTX ranges ("riann:<phase>") for ncu --nvtx. */
 #define RIANN_NPHASES 10
 int riann_timing_phases(riann_ctx *ctx, double *ms, int nphases);
+/* The same split for one timed frame (frame < 0 counts from the last). */
+int riann_timing_phases_frame(riann_ctx *ctx, int64_t frame, double *ms, int nphases);
 const char *riann_phase_name(int k);
 /* Snapshot / restore of the device-resident stream state (previous field and
  * previous units), e.g. to replay the same frames; one snapshot per context. */

@@ -72,6 +72,7 @@ SIGNATURES = {
     "riann_timing_enable": (i32, [P, i32]),
     "riann_timing_read": (i32, [P, P, C.POINTER(u64), C.POINTER(u64)]),
     "riann_timing_phases": (i32, [P, P, i32]),
+    "riann_timing_phases_frame": (i32, [P, i64, P, i32]),
     "riann_phase_name": (C.c_char_p, [i32]),
     "riann_frame_units": (i32, [P, P, i32, i32, i32, P, P]),
     "riann_normalize_rows": (i32, [P, P, i64, i32, P, P]),

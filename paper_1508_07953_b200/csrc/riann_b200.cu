@@ -257,6 +257,7 @@ struct riann_ctx {
     std::vector<std::pair<int, cudaEvent_t>> marks;
     std::vector<std::vector<std::pair<int, cudaEvent_t>>> marks_pending;
     double t_phase[RIANN_NPHASES] = {};
+    std::vector<std::array<double, RIANN_NPHASES>> t_phase_frames;  // per timed frame
     bool nvtx_open = false;
 
     cudaEvent_t ev()
@@ -1666,6 +1667,7 @@ int riann_timing_enable(riann_ctx *c, int on)
     for (auto &m : c->marks) c->ev_pool.push_back(m.second);
     c->marks.clear();
     for (double &x : c->t_phase) x = 0.0;
+    c->t_phase_frames.clear();
     c->timing = on != 0;
     c->t_ms[0] = c->t_ms[1] = c->t_ms[2] = 0.0;
     c->t_frames = 0;
@@ -1690,11 +1692,16 @@ int riann_timing_read(riann_ctx *c, double *ms3, uint64_t *frames, uint64_t *lau
     c->ev_pending.clear();
     for (auto &f : c->marks_pending) {
         // the stretch between mark i and mark i+1 belongs to mark i's phase
+        std::array<double, RIANN_NPHASES> fr{};
         for (size_t i = 0; i + 1 < f.size(); i++) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, f[i].second, f[i + 1].second));
-            if (f[i].first >= 0) c->t_phase[f[i].first] += ms;
+            if (f[i].first >= 0) {
+                c->t_phase[f[i].first] += ms;
+                fr[f[i].first] += ms;
+            }
         }
+        c->t_phase_frames.push_back(fr);
         for (auto &m : f) c->ev_pool.push_back(m.second);
     }
     c->marks_pending.clear();
@@ -1709,6 +1716,16 @@ int riann_timing_phases(riann_ctx *c, double *ms, int nphases)
 {
     RET(riann_timing_read(c, nullptr, nullptr, nullptr));
     for (int k = 0; k < nphases && k < RIANN_NPHASES; k++) ms[k] = c->t_phase[k];
+    return 0;
+}
+
+int riann_timing_phases_frame(riann_ctx *c, int64_t frame, double *ms, int nphases)
+{
+    RET(riann_timing_read(c, nullptr, nullptr, nullptr));
+    const int64_t nf = (int64_t)c->t_phase_frames.size();
+    if (frame < 0) frame += nf;
+    if (frame < 0 || frame >= nf) return fail(RIANN_E_INDEX, "timed frame %lld of %lld", (long long)frame, (long long)nf);
+    for (int k = 0; k < nphases && k < RIANN_NPHASES; k++) ms[k] = c->t_phase_frames[(size_t)frame][k];
     return 0;
 }
 

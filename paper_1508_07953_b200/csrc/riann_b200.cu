@@ -543,7 +543,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
         tmark(c, PH_P0B);
         {
             const int wpb = RIANN_P0_WPB;
-            const size_t smem = (size_t)wpb * rb::p0_words(n) * 4;
+            const size_t smem = (size_t)wpb * rb::p0_smem_words(n) * 4;
             auto k = rb::bulk_p0_kernel<D>;
             CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int bps = 0;

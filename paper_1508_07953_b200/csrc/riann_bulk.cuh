@@ -182,6 +182,12 @@ __device__ __forceinline__ int bit_at(const uint8_t *bits, int64_t e) { return (
 // fall in one short run of the slot.  Part B (j >= n/2) starts at the next
 // multiple of 8 after part A.
 __host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 4095) / 4096) * 128); }
+// per-warp shared words: the n-bit bitmap, at least 8 KB (the radix path's buffers)
+__host__ __device__ constexpr int p0_smem_words(int64_t n) { return p0_words(n) > 2048 ? p0_words(n) : 2048; }
+#ifndef RIANN_P0_RADIX_CAP
+#define RIANN_P0_RADIX_CAP 1024
+#endif
+constexpr int P0_RADIX_CAP = RIANN_P0_RADIX_CAP;  // windows up to this many entries take the radix path
 
 template <int D>
 __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_kernel(BulkParams P)
@@ -193,10 +199,10 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
     const int64_t n = P.n;
     const int jh = (int)(n >> 1);
     const int NW = p0_words(n);  // multiple of 128
-    uint32_t *bm = smem_w + (size_t)wib * NW;
+    uint32_t *bm = smem_w + (size_t)wib * p0_smem_words(n);
     const int64_t nwarps = (int64_t)gridDim.x * wpb;
     const int64_t gwarp = (int64_t)blockIdx.x * wpb + wib;
-    for (int i = lane; i < NW; i += 32) bm[i] = 0u;
+    for (int i = lane; i < p0_smem_words(n); i += 32) bm[i] = 0u;
     __syncwarp();
     for (int64_t g = gwarp; g < P.Q; g += nwarps) {
         QState *sp = P.st + g;
@@ -213,112 +219,192 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
         const int cS = (int)word(12);
         const int64_t off = (int64_t)((uint64_t)word(2) | ((uint64_t)word(3) << 32));
         const int alloc = (cS + 14 + 127) & ~127;
-        // window of the u16 index row -> bitmap; the aligned span's 16-byte loads
-        // are all issued before any marking (MB per lane per round)
-        int cA = 0;  // entries of part A (j < n/2)
-        {
+        int cA, lenA8, lenB8, gap, below = 0, p_in = 0;
+#ifndef RIANN_P0_RADIX
+#define RIANN_P0_RADIX 1
+#endif
+        if (RIANN_P0_RADIX && cS > 0 && cS <= P0_RADIX_CAP) {
+            // small window: bucket the entries by their high bits (counting sort with
+            // shared-memory cursors), insertion-sort each lane's 8 buckets, copy
+            // out in order -- no n-bit bitmap to scan (the bitmap area is reused
+            // and zeroed again afterwards)
+            uint32_t *cnt = bm;                                             // 256 cursors
+            uint16_t *bst = reinterpret_cast<uint16_t *>(bm + 256);         // 256 bucket starts
+            uint16_t *keys = reinterpret_cast<uint16_t *>(bm + 384);        // P0_RADIX_CAP entries
+            const int bsh = max(0, 24 - __clz((int)(n - 1)));                // bucket = j >> bsh < 256
             const uint16_t *row = P.sidx + (int64_t)p * n;
-            auto mark = [&](uint32_t j) {
-                atomicOr(&bm[j >> 5], 1u << (j & 31));
-                cA += (int)j < jh ? 1 : 0;
-            };
-            const int64_t a0 = (lo + 7) & ~(int64_t)7, a1 = hi & ~(int64_t)7;
-            if (a0 < a1) {
-                constexpr int MB = 8;
-                uint16_t hd = 0xffff, tl = 0xffff;
-                if (lo + lane < a0) hd = __ldg(row + lo + lane);
-                if (a1 + lane < hi) tl = __ldg(row + a1 + lane);
-                for (int64_t base = a0; base < a1; base += 256 * MB) {
-                    uint4 v[MB];
+            for (int64_t k = lo + lane; k < hi; k += 32) atomicAdd(&cnt[(uint32_t)__ldg(row + k) >> bsh], 1u);
+            __syncwarp();
+            {
+                uint32_t v[8], sm = 0;
 #pragma unroll
-                    for (int u = 0; u < MB; u++) {
-                        const int64_t v0 = base + (int64_t)(u * 32 + lane) * 8;
-                        v[u] = v0 < a1 ? __ldg(reinterpret_cast<const uint4 *>(row + v0)) : make_uint4(~0u, ~0u, ~0u, ~0u);
-                    }
-#pragma unroll
-                    for (int u = 0; u < MB; u++) {
-                        const int64_t v0 = base + (int64_t)(u * 32 + lane) * 8;
-                        if (v0 < a1) {
-                            const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[u]);
-#pragma unroll
-                            for (int x = 0; x < 8; x++) mark(e8[x]);
-                        }
-                    }
+                for (int k = 0; k < 8; k++) {
+                    v[k] = cnt[lane * 8 + k];
+                    sm += v[k];
                 }
-                if (lo + lane < a0) mark(hd);
-                if (a1 + lane < hi) mark(tl);
-            } else {
-                for (int64_t k = lo + lane; k < hi; k += 32) mark(__ldg(row + k));
-            }
-        }
-        cA = __reduce_add_sync(FULL, cA);
-        const int lenA8 = (cA + 7) & ~7, lenB8 = (cS - cA + 7) & ~7;
-        const int gap = lenA8 - cA;
-        __syncwarp();
-        // enumerate ascending into the slot, clearing the bitmap; rank and presence of p.
-        // Step t: lane L takes words 128t + 4L .. +3 (one LDS.128); one warp scan per step.
-        uint16_t *slot = P.pool + off;
-        const int wp = p >> 5;
-        int run = 0, below = 0, p_in = 0;
-        for (int t = 0; t < NW; t += 128) {
-            const int w0 = t + 4 * lane;
-            uint4 q4 = *reinterpret_cast<const uint4 *>(bm + w0);
-            const uint32_t any4 = q4.x | q4.y | q4.z | q4.w;
-            if (!__any_sync(FULL, any4 != 0u)) continue;
-            if (any4) *reinterpret_cast<uint4 *>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
-            const int c = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
-            const int inc = warp_incl_scan(c, lane);
-            int o = run + inc - c;
-            if ((wp >> 2) == (w0 >> 2)) {  // this lane holds p's word
-                const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
-                int bb = o;
-                for (int k = 0; k < (wp & 3); k++) bb += __popc(wd[k]);
-                below = bb + __popc(wd[wp & 3] & ((1u << (p & 31)) - 1u));
-                p_in = (wd[wp & 3] >> (p & 31)) & 1u;
-            }
-            if (any4) {
-                bool crossed = w0 * 32 >= jh;
-                uint16_t *dst = slot + o + (crossed ? gap : 0);
-                const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
-                if ((jh & 31) == 0) {
-                    // part boundary on a word boundary: one check per word
+                uint32_t run = (uint32_t)warp_incl_scan((int)sm, lane) - sm;
 #pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        uint32_t word = wd[k];
-                        const uint32_t base = (uint32_t)(w0 + k) * 32u;
-                        if (!crossed && (int)base >= jh && word) {
-                            crossed = true;
-                            dst += gap;
+                for (int k = 0; k < 8; k++) {
+                    bst[lane * 8 + k] = (uint16_t)run;
+                    cnt[lane * 8 + k] = run;
+                    run += v[k];
+                }
+            }
+            __syncwarp();
+            for (int64_t k = lo + lane; k < hi; k += 32) {
+                const uint32_t j = __ldg(row + k);
+                keys[atomicAdd(&cnt[j >> bsh], 1u)] = (uint16_t)j;
+            }
+            __syncwarp();
+            // each lane sorts its buckets (cnt[b] is now the end of bucket b)
+            int ca_l = -1, bl_l = -1;
+            const int jb = jh >> bsh, pb = p >> bsh;
+#pragma unroll 1
+            for (int b = lane * 8; b < lane * 8 + 8; b++) {
+                const int s0 = bst[b], e0 = (int)cnt[b];
+                for (int i = s0 + 1; i < e0; i++) {
+                    const uint16_t key = keys[i];
+                    int j2 = i - 1;
+                    while (j2 >= s0 && keys[j2] > key) {
+                        keys[j2 + 1] = keys[j2];
+                        j2--;
+                    }
+                    keys[j2 + 1] = key;
+                }
+                if (b == jb) {  // entries < n/2 end inside (or at) this bucket
+                    int c = s0;
+                    while (c < e0 && (int)keys[c] < jh) c++;
+                    ca_l = c;
+                }
+                if (b == pb) {
+                    int c = s0;
+                    while (c < e0 && (int)keys[c] < p) c++;
+                    bl_l = c;
+                }
+            }
+            cA = __shfl_sync(FULL, ca_l, jb >> 3);
+            below = __shfl_sync(FULL, bl_l, pb >> 3);
+            lenA8 = (cA + 7) & ~7;
+            lenB8 = (cS - cA + 7) & ~7;
+            gap = lenA8 - cA;
+            p_in = (lo == 0) ? 1 : 0;  // p is rank 0 of its own row (self first, model.py:181-186)
+            __syncwarp();
+            uint16_t *slot = P.pool + off;
+            for (int i = lane; i < cS; i += 32) slot[i < cA ? i : i + gap] = keys[i];
+            __syncwarp();
+            const int used_w = 384 + ((cS + 1) >> 1);
+            for (int w = lane; w < used_w; w += 32) bm[w] = 0u;
+            __syncwarp();
+            RB_CHECK(cA <= cS && lenA8 + lenB8 <= alloc && below <= cS, 11);
+        } else {
+            // window of the u16 index row -> bitmap; the aligned span's 16-byte loads
+            // are all issued before any marking (MB per lane per round)
+            cA = 0;
+            {
+                const uint16_t *row = P.sidx + (int64_t)p * n;
+                auto mark = [&](uint32_t j) {
+                    atomicOr(&bm[j >> 5], 1u << (j & 31));
+                    cA += (int)j < jh ? 1 : 0;
+                };
+                const int64_t a0 = (lo + 7) & ~(int64_t)7, a1 = hi & ~(int64_t)7;
+                if (a0 < a1) {
+                    constexpr int MB = 8;
+                    uint16_t hd = 0xffff, tl = 0xffff;
+                    if (lo + lane < a0) hd = __ldg(row + lo + lane);
+                    if (a1 + lane < hi) tl = __ldg(row + a1 + lane);
+                    for (int64_t base = a0; base < a1; base += 256 * MB) {
+                        uint4 v[MB];
+    #pragma unroll
+                        for (int u = 0; u < MB; u++) {
+                            const int64_t v0 = base + (int64_t)(u * 32 + lane) * 8;
+                            v[u] = v0 < a1 ? __ldg(reinterpret_cast<const uint4 *>(row + v0)) : make_uint4(~0u, ~0u, ~0u, ~0u);
                         }
-                        while (word) {
-                            *dst++ = (uint16_t)(base + (uint32_t)(__ffs(word) - 1));
-                            word &= word - 1;
+    #pragma unroll
+                        for (int u = 0; u < MB; u++) {
+                            const int64_t v0 = base + (int64_t)(u * 32 + lane) * 8;
+                            if (v0 < a1) {
+                                const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[u]);
+    #pragma unroll
+                                for (int x = 0; x < 8; x++) mark(e8[x]);
+                            }
                         }
                     }
+                    if (lo + lane < a0) mark(hd);
+                    if (a1 + lane < hi) mark(tl);
                 } else {
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        uint32_t word = wd[k];
-                        const uint32_t base = (uint32_t)(w0 + k) * 32u;
-                        while (word) {
-                            const int b = __ffs(word) - 1;
-                            word &= word - 1;
-                            const uint32_t j = base + b;
-                            if (!crossed && (int)j >= jh) {
+                    for (int64_t k = lo + lane; k < hi; k += 32) mark(__ldg(row + k));
+                }
+            }
+            cA = __reduce_add_sync(FULL, cA);
+            lenA8 = (cA + 7) & ~7;
+            lenB8 = (cS - cA + 7) & ~7;
+            gap = lenA8 - cA;
+            __syncwarp();
+            // enumerate ascending into the slot, clearing the bitmap; rank and presence of p.
+            // Step t: lane L takes words 128t + 4L .. +3 (one LDS.128); one warp scan per step.
+            uint16_t *slot = P.pool + off;
+            const int wp = p >> 5;
+            int run = 0;
+            for (int t = 0; t < NW; t += 128) {
+                const int w0 = t + 4 * lane;
+                uint4 q4 = *reinterpret_cast<const uint4 *>(bm + w0);
+                const uint32_t any4 = q4.x | q4.y | q4.z | q4.w;
+                if (!__any_sync(FULL, any4 != 0u)) continue;
+                if (any4) *reinterpret_cast<uint4 *>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+                const int c = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
+                const int inc = warp_incl_scan(c, lane);
+                int o = run + inc - c;
+                if ((wp >> 2) == (w0 >> 2)) {  // this lane holds p's word
+                    const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
+                    int bb = o;
+                    for (int k = 0; k < (wp & 3); k++) bb += __popc(wd[k]);
+                    below = bb + __popc(wd[wp & 3] & ((1u << (p & 31)) - 1u));
+                    p_in = (wd[wp & 3] >> (p & 31)) & 1u;
+                }
+                if (any4) {
+                    bool crossed = w0 * 32 >= jh;
+                    uint16_t *dst = slot + o + (crossed ? gap : 0);
+                    const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
+                    if ((jh & 31) == 0) {
+                        // part boundary on a word boundary: one check per word
+    #pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            uint32_t word = wd[k];
+                            const uint32_t base = (uint32_t)(w0 + k) * 32u;
+                            if (!crossed && (int)base >= jh && word) {
                                 crossed = true;
                                 dst += gap;
                             }
-                            *dst++ = (uint16_t)j;
+                            while (word) {
+                                *dst++ = (uint16_t)(base + (uint32_t)(__ffs(word) - 1));
+                                word &= word - 1;
+                            }
+                        }
+                    } else {
+    #pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            uint32_t word = wd[k];
+                            const uint32_t base = (uint32_t)(w0 + k) * 32u;
+                            while (word) {
+                                const int b = __ffs(word) - 1;
+                                word &= word - 1;
+                                const uint32_t j = base + b;
+                                if (!crossed && (int)j >= jh) {
+                                    crossed = true;
+                                    dst += gap;
+                                }
+                                *dst++ = (uint16_t)j;
+                            }
                         }
                     }
                 }
+                run += __shfl_sync(FULL, inc, 31);
             }
-            run += __shfl_sync(FULL, inc, 31);
+            const int lp = (wp >> 2) & 31;
+            below = __shfl_sync(FULL, below, lp);
+            p_in = __shfl_sync(FULL, p_in, lp);
+            RB_CHECK(run == cS && cA <= cS && lenA8 + lenB8 <= alloc && below <= cS, 10);
         }
-        const int lp = (wp >> 2) & 31;
-        below = __shfl_sync(FULL, below, lp);
-        p_in = __shfl_sync(FULL, p_in, lp);
-        RB_CHECK(run == cS && cA <= cS && lenA8 + lenB8 <= alloc && below <= cS, 10);
         // alive bits of the list (both buffers zero past the list end, whole words)
         {
             const int nb = (lenA8 + lenB8) >> 3, nbw = alloc >> 3;

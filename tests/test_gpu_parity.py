@@ -512,3 +512,29 @@ def test_many_used_anchors_inside_s(R, oracle_mod):
         assert r["distance_evals"] == res["evals"][i] and r["candidates_final"] == res["cand"][i], i
         assert np.array_equal(r["scanned"], res["scanned"][i]), i
     assert (res["rings"] == 50).all()  # first ring + 49 draws: prev is a used copy too
+
+
+@pytest.mark.parametrize("n", [4112, 8208])
+def test_bulk_path_unaligned_half(R, oracle_mod, n):
+    """n % 16 == 0 but n/2 not a multiple of the P0b bucket width nor of 32
+    (n = 4,112: n/2 = 2,056): the part-A/B split falls inside a bucket of the
+    radix path and inside a bitmap word of the bitmap path.  Whole frames vs
+    the oracle, bit for bit."""
+    from dataclasses import replace
+
+    from paper_1508_07953_b200 import workloads as W
+
+    cfg = replace(W.CONFIGS[1], height=72, width=96, frames=3, n_refs=n)
+    clip = W.clip(cfg)
+    refs = W.reference_set(cfg)
+    model = R.ReferenceModel.from_refs(refs, cfg.patch)
+    om = oracle_mod.OracleModel.build(refs)
+    gw, gh = cfg.grid
+    prev = oracle_mod.init_field_indices(gw, gh, n, 0)
+    prev_unit = None
+    for t, (_, fld, st) in enumerate(R.stream_fields(model, clip)):
+        idx, dist, ost, unit = oracle_mod.process_frame(om, clip[t], prev, cfg.patch, t + 1, prev_unit=prev_unit)
+        assert np.array_equal(fld.indices, idx), t
+        assert np.array_equal(_bits(fld.distances), _bits(dist)), t
+        assert st.total_rings == ost["total_rings"] and st.total_distance_evals == ost["total_distance_evals"]
+        prev, prev_unit = idx, unit

@@ -47,8 +47,8 @@
 #ifndef RIANN_FILTER_MINB
 #define RIANN_FILTER_MINB 3
 #endif
-#ifndef RIANN_FILTER_LCAP
-#define RIANN_FILTER_LCAP 8192
+#ifndef RIANN_FILTER_ROUNDS
+#define RIANN_FILTER_ROUNDS 2
 #endif
 #ifndef RIANN_WIN_MINB
 #define RIANN_WIN_MINB 4
@@ -70,7 +70,6 @@ constexpr int FCAP = RIANN_FCAP;  // query descriptors per filter stage
 #define RIANN_FILTER_WARPS 16
 #endif
 constexpr int FW2 = RIANN_FILTER_WARPS;  // warps per filter CTA
-constexpr int LCAP = RIANN_FILTER_LCAP;  // list entries per filter sub-chunk
 #ifndef RIANN_FDIRECT
 #define RIANN_FDIRECT 64
 #endif
@@ -405,6 +404,17 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
             p_in = __shfl_sync(FULL, p_in, lp);
             RB_CHECK(run == cS && cA <= cS && lenA8 + lenB8 <= alloc && below <= cS, 10);
         }
+        // padding entries are valid indices of their part (the filter looks every
+        // entry of a group up, alive or not)
+        {
+            uint16_t *slot = P.pool + off;
+            if (lane < 8) {
+                if (cA + lane < lenA8) slot[cA + lane] = 0;
+            } else if (lane < 16) {
+                const int i = lenA8 + (cS - cA) + (lane - 8);
+                if (i < lenA8 + lenB8) slot[i] = (uint16_t)jh;
+            }
+        }
         // alive bits of the list (both buffers zero past the list end, whole words)
         {
             const int nb = (lenA8 + lenB8) >> 3, nbw = alloc >> 3;
@@ -530,20 +540,20 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigne
 // ~30 ns of TMA issue per copy: measured slower.)
 __host__ __device__ constexpr size_t filter_smem(int64_t n)
 {
-    return (size_t)n + 2 * FCAP * 16 + (FCAP + 1) * 4;
+    return (size_t)n + 2 * FCAP * 16 + (FCAP + 1) * 4 + FCAP + 4;
 }
 
 __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kernel(BulkParams P, int cur)
 {
     extern __shared__ __align__(128) unsigned char smem_f[];
-    constexpr int NPRE = LCAP / 8 / (FW2 * 32);  // staged groups per thread
     const int64_t n = P.n;
     const int jh = (int)(n >> 1);
     uint16_t *row = reinterpret_cast<uint16_t *>(smem_f);
     int4 *descb = reinterpret_cast<int4 *>(smem_f + n);
-    int *qg0 = reinterpret_cast<int *>(descb + 2 * FCAP);
+    int *qg0 = reinterpret_cast<int *>(descb + 2 * FCAP);  // group offsets of the chunk's queries with groups in part h
+    uint8_t *qsel = reinterpret_cast<uint8_t *>(qg0 + FCAP + 1);  // ... and their descriptor slots
     __shared__ uint64_t dbar[2], rbar;
-    __shared__ int s_it[2], s_cnt[2], s_start[2], s_ng, s_direct;
+    __shared__ int s_it[2], s_cnt[2], s_start[2], s_ng, s_mc, s_direct;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint8_t *bcur = cur ? P.bits1 : P.bits0;
     uint8_t *bnxt = cur ? P.bits0 : P.bits1;
@@ -627,9 +637,10 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                 mbar_wait(&dbar[1], dpar1);
                 dpar1 ^= 1;
             }
-            // warp 0: group offsets of the chunk's queries (part h) and the row copy
+            // warp 0: group offsets of the chunk's queries that have groups in
+            // part h (compacted: offsets strictly ascending) and the row copy
             if (w == 0) {
-                int run = 0;
+                int run = 0, mc = 0;
                 for (int b = 0; b < m; b += 32) {
                     const int i = b + lane;
                     int ng = 0;
@@ -638,12 +649,19 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
                         ng = h ? (d.w >> 17) : (d.z >> 17);
                     }
                     const int inc = warp_incl_scan(ng, lane);
-                    if (i < m) qg0[i] = run + inc - ng;
+                    const unsigned nz = __ballot_sync(FULL, ng > 0);
+                    if (ng > 0) {
+                        const int o = mc + __popc(nz & lanemask_lt());
+                        qg0[o] = run + inc - ng;
+                        qsel[o] = (uint8_t)i;
+                    }
+                    mc += __popc(nz);
                     run += __shfl_sync(FULL, inc, 31);
                 }
                 if (lane == 0) {
-                    qg0[m] = run;
+                    qg0[mc] = run;
                     s_ng = run;
+                    s_mc = mc;
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     if (first_sub) {
                         // few list groups for this (anchor, half): look the ranks up in
@@ -659,99 +677,129 @@ __global__ void __launch_bounds__(FW2 * 32, RIANN_FILTER_MINB) bulk_filter_kerne
             }
             __syncthreads();
             const int NGt = s_ng;
-            // sub-chunks of GC groups; a query's groups may span sub-chunks
-            constexpr int GC = NPRE * FW2 * 32;
-            bool ran = false;  // block-uniform (NGt, first_sub are)
-            for (int G0 = 0; G0 < NGt || (first_sub && G0 == 0); G0 += GC) {
-                ran = true;
-                const int NG = min(GC, NGt - G0);
-                // list groups and alive bytes of my groups (independent of the row copy)
-                uint32_t al[NPRE];
-                int qi[NPRE];
-                int64_t eb[NPRE];
-                uint4 v[NPRE];
-#pragma unroll
-                for (int k = 0; k < NPRE; k++) {
-                    const int G = G0 + k * FW2 * 32 + tid;
-                    qi[k] = -1;
-                    al[k] = 0;
-                    eb[k] = 0;
-                    v[k] = make_uint4(0u, 0u, 0u, 0u);
-                    if (G < G0 + NG) {
-                        int x = 0, r = m;  // last query with qg0 <= G
-                        while (r - x > 1) {
-                            const int mid = (x + r) >> 1;
-                            if (qg0[mid] <= G) x = mid;
-                            else r = mid;
-                        }
-                        const int4 d = desc[x];
-                        RB_CHECK(x < m && d.x >= 0 && d.x < P.Q, 20);
-                        qi[k] = x;
-                        eb[k] = ((int64_t)(uint32_t)d.y << 7) + (h ? ((d.z >> 17) << 3) : 0) + (int64_t)(G - qg0[x]) * 8;
-                        RB_CHECK(eb[k] >= 0 && eb[k] + 8 <= P.pool_cap, 21);
-                        al[k] = bcur[eb[k] >> 3];
-                        v[k] = *reinterpret_cast<const uint4 *>(P.pool + eb[k]);
-                    }
+            const bool direct = s_direct != 0;  // block-uniform, set with s_ng
+            // the next item and its descriptors, while the copies fly
+            if (first_sub && w == 1) {
+                int nit, ncnt, nstart;
+                next_item(nit, ncnt, nstart);
+                if (lane == 0) {
+                    s_it[db ^ 1] = nit;
+                    s_cnt[db ^ 1] = ncnt;
+                    s_start[db ^ 1] = nstart;
+                    if (nit >= 0) fetch_desc(db ^ 1, nstart, min(ncnt, FCAP));
                 }
-                // the next item and its descriptors, while the copies fly
-                if (first_sub && c0 == 0 && w == 1) {
-                    int nit, ncnt, nstart;
-                    next_item(nit, ncnt, nstart);
-                    if (lane == 0) {
-                        s_it[db ^ 1] = nit;
-                        s_cnt[db ^ 1] = ncnt;
-                        s_start[db ^ 1] = nstart;
-                        if (nit >= 0) fetch_desc(db ^ 1, nstart, min(ncnt, FCAP));
-                    }
-                }
-                const bool direct = s_direct != 0;  // block-uniform, set with s_ng
-                if (first_sub && !direct) {
-                    mbar_wait(&rbar, rpar);
-                    rpar ^= 1;
-                }
-                const uint32_t hoff = (uint32_t)(h * jh), jmax = (uint32_t)(jh - 1);
-                const uint16_t *grow = P.pos + (int64_t)a * n + (int64_t)h * jh;
-#pragma unroll
-                for (int k = 0; k < NPRE; k++) {
-                    if (k * FW2 * 32 >= NG) break;  // block-uniform
-                    uint32_t keep = 0;
-                    int gq = -1;
-                    if (qi[k] >= 0) {
-                        const int4 d = desc[qi[k]];
-                        gq = d.x;
-                        const uint32_t lo = (uint32_t)(d.z & 0x1ffff), wlen = (uint32_t)(d.w & 0x1ffff) - lo;
-                        const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[k]);
-                        // all eight lookups issued unconditionally (padding / dead entries
-                        // clamped into the half row), the alive bits mask the result
-                        uint32_t rk[8];
-                        if (direct) {
-#pragma unroll
-                            for (int x = 0; x < 8; x++) rk[x] = __ldg(grow + min((uint32_t)e8[x] - hoff, jmax));
-                        } else {
-#pragma unroll
-                            for (int x = 0; x < 8; x++) rk[x] = row[min((uint32_t)e8[x] - hoff, jmax)];
-                        }
-#pragma unroll
-                        for (int x = 0; x < 8; x++)
-                            keep |= (rk[x] - lo < wlen ? 1u : 0u) << x;  // lo <= r < hi
-                        keep &= al[k];
-                        bnxt[eb[k] >> 3] = (uint8_t)keep;
-                    }
-                    const int q_l0 = __shfl_sync(FULL, qi[k], 0);
-                    const int c = __popc(keep);
-                    if (__all_sync(FULL, qi[k] == q_l0)) {
-                        const int cw = __reduce_add_sync(FULL, c);
-                        if (lane == 0 && q_l0 >= 0 && cw > 0) atomicAdd(P.kept + gq, cw);
-                    } else if (qi[k] >= 0 && c > 0) {
-                        atomicAdd(P.kept + gq, c);
-                    }
-                }
-                first_sub = false;
-                __syncthreads();
             }
-            // no sub-chunk ran: every warp must have read s_ng / qg0 before
-            // warp 0 rewrites them for the next chunk
-            if (!ran) __syncthreads();
+            // The chunk's NGt list groups are cut into FW2 contiguous spans of whole
+            // 32-group rounds, one per warp; lane l of a round takes group Gr + l.
+            // Its query: xc (the query holding Gr, warp-uniform) plus the number of
+            // query boundaries in (Gr, Gr + l], a popcount over a 32-bit boundary
+            // mask (the compacted offsets are strictly ascending, so at most 31
+            // boundaries fall inside a round).  FR rounds are loaded before any is
+            // tested.
+            const int mc = s_mc;
+            const int rpw = ((NGt + 31) / 32 + FW2 - 1) / FW2;  // rounds per warp
+            const int gs = min(w * rpw * 32, NGt), ge = min(gs + rpw * 32, NGt);
+            bool need_row = first_sub && !direct;  // block-uniform
+            if (need_row) rpar ^= 1;
+            const uint32_t hoff = (uint32_t)(h * jh), jmax = (uint32_t)(jh - 1);
+            (void)jmax;
+            const uint16_t *grow = P.pos + (int64_t)a * n;            // direct lookups: pos[a][e]
+            const uint32_t rowb = smem_addr(row) - 2u * hoff;         // staged half row: byte address of entry e = rowb + 2 e
+            if (gs < ge) {
+                int xc;  // last compacted query with qg0[xc] <= gs
+                {
+                    const unsigned b1 = __ballot_sync(FULL, lane * 8 <= mc && qg0[min(lane * 8, mc)] <= gs);
+                    const int blk = 31 - __clz((int)b1);
+                    const int i1 = blk * 8 + (lane & 7);
+                    const unsigned b2 = __ballot_sync(FULL, lane < 8 && i1 <= mc && qg0[min(i1, mc)] <= gs);
+                    xc = blk * 8 + 31 - __clz((int)b2);
+                }
+                constexpr int FR = RIANN_FILTER_ROUNDS;
+                const uint32_t le_mask = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
+                for (int Gb = gs; Gb < ge; Gb += 32 * FR) {
+                    uint4 v[FR];
+                    uint32_t al[FR];
+                    uint32_t eg[FR];  // list group (8 entries) in the pool
+                    int dsl[FR];  // descriptor slot, -1: no group
+#pragma unroll
+                    for (int r = 0; r < FR; r++) {
+                        const int Gr = Gb + 32 * r;
+                        dsl[r] = -1;
+                        al[r] = 0;
+                        eg[r] = 0;
+                        v[r] = make_uint4(0u, 0u, 0u, 0u);
+                        if (Gr < ge) {  // warp-uniform
+                            const int bo = qg0[min(xc + 1 + lane, mc)] - Gr;  // >= 1, ascending over the lanes
+                            const uint32_t bm = __reduce_or_sync(FULL, bo < 32 ? 1u << bo : 0u);
+                            const int xl = xc + __popc(bm & le_mask);
+                            xc += __popc(bm) + (__any_sync(FULL, bo == 32) ? 1 : 0);  // the query holding Gr + 32
+                            const int Gl = Gr + lane;
+                            if (Gl < ge) {
+                                const int di = qsel[xl];
+                                const int4 d = desc[di];
+                                RB_CHECK(xl < mc && di < m && d.x >= 0 && d.x < P.Q && Gl >= qg0[xl] && Gl < qg0[xl + 1], 20);
+                                dsl[r] = di;
+                                eg[r] = ((uint32_t)d.y << 4) + (h ? (uint32_t)(d.z >> 17) : 0u) + (uint32_t)(Gl - qg0[xl]);
+                                RB_CHECK((int64_t)eg[r] * 8 + 8 <= P.pool_cap, 21);
+                                al[r] = bcur[eg[r]];
+                                v[r] = reinterpret_cast<const uint4 *>(P.pool)[eg[r]];
+                            }
+                        }
+                    }
+                    if (need_row) {  // the first test of the item waits for the row copy
+                        mbar_wait(&rbar, rpar ^ 1);
+                        need_row = false;
+                    }
+#pragma unroll
+                    for (int r = 0; r < FR; r++) {
+                        if (Gb + 32 * r >= ge) break;  // warp-uniform
+                        uint32_t keep = 0;
+                        int gq = -1;
+                        if (dsl[r] >= 0) {
+                            const int4 d = desc[dsl[r]];
+                            gq = d.x;
+                            const uint32_t lo = (uint32_t)(d.z & 0x1ffff), wlen = (uint32_t)(d.w & 0x1ffff) - lo;
+                            // all eight lookups issued unconditionally, the alive bits mask the
+                            // result: dead and padding entries are indices of this half too (P0b)
+                            const uint32_t w4[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
+                            uint32_t rk[8];
+                            if (direct) {
+#pragma unroll
+                                for (int k = 0; k < 8; k++) {
+                                    const uint32_t e = (k & 1) ? (w4[k >> 1] >> 16) : (w4[k >> 1] & 0xffffu);
+                                    RB_CHECK(e - hoff <= jmax, 22);
+                                    rk[k] = __ldg(grow + e);
+                                }
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < 8; k++) {
+                                    const uint32_t e = (k & 1) ? (w4[k >> 1] >> 16) : (w4[k >> 1] & 0xffffu);
+                                    RB_CHECK(e - hoff <= jmax, 22);
+                                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(rk[k]) : "r"(rowb + 2u * e));
+                                }
+                            }
+#pragma unroll
+                            for (int k = 0; k < 8; k++) keep |= (rk[k] - lo < wlen ? 1u : 0u) << k;  // lo <= r < hi
+                            keep &= al[r];
+                            bnxt[eg[r]] = (uint8_t)keep;
+                        }
+                        const int c = __popc(keep);
+                        const int q_l0 = __shfl_sync(FULL, gq, 0);
+                        if (__all_sync(FULL, gq == q_l0)) {
+                            const int cw = __reduce_add_sync(FULL, c);
+                            if (lane == 0 && cw > 0) atomicAdd(P.kept + gq, cw);
+                        } else if (c > 0) {
+                            atomicAdd(P.kept + gq, c);
+                        }
+                    }
+                }
+            }
+            // a warp without work still observes the copy: no row copy is in flight
+            // when the next one is issued
+            if (need_row) mbar_wait(&rbar, rpar ^ 1);
+            first_sub = false;
+            // every warp is done with the descriptors, qg0 and the row before they are rewritten
+            __syncthreads();
         }
         db ^= 1;
     }

@@ -1315,17 +1315,12 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                 lp += FSEG;
             }
             __syncwarp();
-            // chunk 0 over the block: a lane pair per candidate, each lane one
-            // 16-byte half of its 32-byte chunk (one L1 wavefront per candidate)
+            // chunk 0 over the block: a lane per candidate, one 32-byte load each
+            // (one L1 wavefront per candidate); later chunks: a lane pair per
+            // survivor, each lane one 16-byte half of the 32-byte chunk
             const int hh = lane & 1;
             const unsigned EVEN = 0x55555555u;
             float qc[8];
-            {
-                const float4 *q4 = reinterpret_cast<const float4 *>(qp) + 2 * hh;
-                const float4 va = __ldg(q4), vb = __ldg(q4 + 1);
-                qc[0] = va.x; qc[1] = va.y; qc[2] = va.z; qc[3] = va.w;
-                qc[4] = vb.x; qc[5] = vb.y; qc[6] = vb.z; qc[7] = vb.w;
-            }
             auto part = [&](const uint4 &v) {
                 float s = 0.f;
                 const __half2 *h2 = reinterpret_cast<const __half2 *>(&v);
@@ -1339,33 +1334,63 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                 return __fadd_rn(s, __shfl_xor_sync(FULL, s, 1));
             };
             int nA = 0;
-            // FU rounds of 16 candidates per iteration, their loads issued together
-#ifndef RIANN_FINAL_FU
-#define RIANN_FINAL_FU 4
-#endif
-            constexpr int FU = RIANN_FINAL_FU;
-            for (int e0 = 0; e0 < bn; e0 += 16 * FU) {
-                uint4 v[FU];
-                uint32_t jj[FU];
+            {
+                float q0[16];
+                {
+                    const float4 *q4 = reinterpret_cast<const float4 *>(qp);
 #pragma unroll
-                for (int u = 0; u < FU; u++) {
-                    const int e = e0 + 16 * u + (lane >> 1);
-                    jj[u] = Cj[e < bn ? e : 0];
-                    v[u] = ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + pca_chunk_off(jj[u], 0, P.n, D)) + hh,
-                                     pol_keep);
-                }
-#pragma unroll
-                for (int u = 0; u < FU; u++) {
-                    const int e = e0 + 16 * u + (lane >> 1);
-                    const float s = part(v[u]);
-                    const bool keep = e < bn && s <= thr;
-                    const unsigned ball = __ballot_sync(FULL, keep) & EVEN;
-                    if (keep && hh == 0) {
-                        const int o = nA + __popc(ball & lanemask_lt());
-                        Aj[o] = jj[u];
-                        As[o] = s;
+                    for (int x = 0; x < 4; x++) {
+                        const float4 t = __ldg(q4 + x);
+                        q0[4 * x] = t.x; q0[4 * x + 1] = t.y; q0[4 * x + 2] = t.z; q0[4 * x + 3] = t.w;
                     }
-                    nA += __popc(ball);
+                }
+                auto part16 = [&](const uint4 &va, const uint4 &vb) {
+                    float s = 0.f;
+                    const __half2 *ha = reinterpret_cast<const __half2 *>(&va);
+                    const __half2 *hb = reinterpret_cast<const __half2 *>(&vb);
+#pragma unroll
+                    for (int x = 0; x < 4; x++) {
+                        const float2 f = __half22float2(ha[x]);
+                        const float a0 = __fsub_rn(f.x, q0[2 * x]), a1 = __fsub_rn(f.y, q0[2 * x + 1]);
+                        s = __fmaf_rn(a0, a0, s);
+                        s = __fmaf_rn(a1, a1, s);
+                    }
+#pragma unroll
+                    for (int x = 0; x < 4; x++) {
+                        const float2 f = __half22float2(hb[x]);
+                        const float a0 = __fsub_rn(f.x, q0[8 + 2 * x]), a1 = __fsub_rn(f.y, q0[8 + 2 * x + 1]);
+                        s = __fmaf_rn(a0, a0, s);
+                        s = __fmaf_rn(a1, a1, s);
+                    }
+                    return s;
+                };
+                // FU rounds of 32 candidates per iteration, their loads issued together
+#ifndef RIANN_FINAL_FU
+#define RIANN_FINAL_FU 2
+#endif
+                constexpr int FU = RIANN_FINAL_FU;
+                for (int e0 = 0; e0 < bn; e0 += 32 * FU) {
+                    uint4 va[FU], vb[FU];
+                    uint32_t jj[FU];
+#pragma unroll
+                    for (int u = 0; u < FU; u++) {
+                        const int e = e0 + 32 * u + lane;
+                        jj[u] = Cj[e < bn ? e : 0];
+                        ld_keep32(SP.refs_pca16 + pca_chunk_off(jj[u], 0, P.n, D), pol_keep, va[u], vb[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < FU; u++) {
+                        const int e = e0 + 32 * u + lane;
+                        const float s = part16(va[u], vb[u]);
+                        const bool keep = e < bn && s <= thr;
+                        const unsigned ball = __ballot_sync(FULL, keep);
+                        if (keep) {
+                            const int o = nA + __popc(ball & lanemask_lt());
+                            Aj[o] = jj[u];
+                            As[o] = s;
+                        }
+                        nA += __popc(ball);
+                    }
                 }
             }
             __syncwarp();

@@ -495,6 +495,13 @@ __device__ __forceinline__ uint4 ld_keep16(const uint4 *a, uint64_t pol)
                  : "l"(a), "l"(pol));
     return v;
 }
+// one 32-byte sector per lane (sm_100: 256-bit global loads)
+__device__ __forceinline__ void ld_keep32(const void *a, uint64_t pol, uint4 &lo, uint4 &hi)
+{
+    asm("ld.global.nc.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+        : "l"(a), "l"(pol));
+}
 // streamed once (candidate lists): no L1 allocation, evict first from L2
 __device__ __forceinline__ uint4 ld_once16(const uint4 *a, uint64_t pol)
 {

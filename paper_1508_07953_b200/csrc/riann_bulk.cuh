@@ -1320,8 +1320,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
             // survivor, each lane one 16-byte half of the 32-byte chunk
             const int hh = lane & 1;
             const unsigned EVEN = 0x55555555u;
-            float qc[8];
-            auto part = [&](const uint4 &v) {
+            auto part = [&](const uint4 &v, const float (&qc)[8]) {
                 float s = 0.f;
                 const __half2 *h2 = reinterpret_cast<const __half2 *>(&v);
 #pragma unroll
@@ -1394,24 +1393,41 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                 }
             }
             __syncwarp();
-            // further chunks for the candidates still alive
-            for (int c = 1; c < NCH && nA > 0; c++) {
-                {
-                    const float4 *q4 = reinterpret_cast<const float4 *>(qp + 16 * c) + 2 * hh;
-                    const float4 va = __ldg(q4), vb = __ldg(q4 + 1);
-                    qc[0] = va.x; qc[1] = va.y; qc[2] = va.z; qc[3] = va.w;
-                    qc[4] = vb.x; qc[5] = vb.y; qc[6] = vb.z; qc[7] = vb.w;
+            // further chunks for the candidates still alive, FCW chunks per step
+            // (partial sums only grow: one test after the step's last chunk)
+#ifndef RIANN_FINAL_CW
+#define RIANN_FINAL_CW 2
+#endif
+            constexpr int FCW = RIANN_FINAL_CW;
+            for (int c = 1; c < NCH && nA > 0; c += FCW) {
+                const int cn = min(FCW, NCH - c);
+                float qcs[FCW][8];
+#pragma unroll
+                for (int k = 0; k < FCW; k++) {
+                    if (k < cn) {
+                        const float4 *q4 = reinterpret_cast<const float4 *>(qp + 16 * (c + k)) + 2 * hh;
+                        const float4 va = __ldg(q4), vb = __ldg(q4 + 1);
+                        qcs[k][0] = va.x; qcs[k][1] = va.y; qcs[k][2] = va.z; qcs[k][3] = va.w;
+                        qcs[k][4] = vb.x; qcs[k][5] = vb.y; qcs[k][6] = vb.z; qcs[k][7] = vb.w;
+                    }
                 }
-                const bool last = c == NCH - 1;
+                const bool last = c + cn == NCH;
                 int nB = 0;
                 for (int i0 = 0; i0 < nA; i0 += 16) {
                     const int i = i0 + (lane >> 1);
                     const bool valid = i < nA;
                     const uint32_t j = valid ? Aj[i] : Aj[0];
                     const float s0 = valid ? As[i] : 0.f;
-                    const uint4 v =
-                        ld_keep16(reinterpret_cast<const uint4 *>(SP.refs_pca16 + pca_chunk_off(j, c, P.n, D)) + hh, pol_keep);
-                    const float s = __fadd_rn(s0, part(v));
+                    uint4 v[FCW];
+#pragma unroll
+                    for (int k = 0; k < FCW; k++)
+                        if (k < cn)
+                            v[k] = ld_keep16(
+                                reinterpret_cast<const uint4 *>(SP.refs_pca16 + pca_chunk_off(j, c + k, P.n, D)) + hh, pol_keep);
+                    float s = s0;
+#pragma unroll
+                    for (int k = 0; k < FCW; k++)
+                        if (k < cn) s = __fadd_rn(s, part(v[k], qcs[k]));
                     if (!last) {
                         const bool keep = valid && s <= thr;
                         const unsigned ball = __ballot_sync(FULL, keep) & EVEN;

@@ -420,6 +420,7 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
     B.coarse = c->coarse.as<float>();
     B.coarse1 = c->coarse1.as<float>();
     B.cs1 = c->cs1;
+    B.vec_probe = (c->cs1 % 4 == 0 && c->ncoarse % 4 == 0 && n % 64 == 0) ? 1 : 0;
     B.n = n;
     B.ncoarse = c->ncoarse;
     B.units = Pq.units;

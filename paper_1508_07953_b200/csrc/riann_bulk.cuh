@@ -109,6 +109,7 @@ struct BulkParams {
     const float *coarse1;    // coarse1[a][k] = coarse[a][k*cs1] (k < 32; +inf past the row)
     int64_t n;
     int ncoarse, cs1;
+    int vec_probe;           // window search with 16-byte probes (cs1 % 4 == 0, ncoarse % 4 == 0, n % 64 == 0)
     const float *units;
     const int32_t *prev;
     int64_t Q;
@@ -168,6 +169,22 @@ __device__ __forceinline__ void rng_store(QState &s, const Pcg64 &r)
     s.il = r.il;
     s.rng_has = r.has;
     s.rng_buf = r.buf;
+}
+
+// position of the set bit of rank r (0-based, r < popc(w)): five popcount halvings
+// (__fns is a software loop)
+__device__ __forceinline__ int nth_bit(uint32_t w, int r)
+{
+    int pos = 0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const int c = __popc(w & ((1u << s) - 1u));
+        const bool up = r >= c;
+        r -= up ? c : 0;
+        pos += up ? s : 0;
+        w = up ? (w >> s) : w;
+    }
+    return pos;
 }
 
 __device__ __forceinline__ int bit_at(const uint8_t *bits, int64_t e) { return (bits[e >> 3] >> (e & 7)) & 1; }
@@ -873,6 +890,64 @@ __device__ __forceinline__ double dist_window8(const BulkParams &P, int a, const
     const bool sh = gl >= 4;
     const int sl = gl & 3;
     const double thr = sh ? hv : lv;
+    int res;
+    if (P.vec_probe) {
+        // 16-byte probes of aligned blocks (cs1 % 4 == 0, nb % 4 == 0, n % 64 == 0).
+        // The level-1 block's first coarse entry (coarse1[b1 - 1]) is known to
+        // pass, the next block's first entry to fail, so counting the aligned 32
+        // entries [cb, cb + 32) gives b directly; the same one level down.
+        int b;
+        {
+            const int b1 = sh ? b1hi : b1lo;
+            const int cb = (b1 - 1) * cs1;
+            int cnt = 0;
+            if (act && b1 > 0) {
+                const int cend = min(b1 * cs1, nb);
+                const float *cr = P.coarse + (int64_t)a * nb;
+                float4 c4[2];
+#pragma unroll
+                for (int x = 0; x < 2; x++) {
+                    const int ci = cb + sl * 8 + 4 * x;
+                    c4[x] = ci < cend ? __ldg(reinterpret_cast<const float4 *>(cr + ci)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int x = 0; x < 2; x++) {
+                    const int ci = cb + sl * 8 + 4 * x;
+                    const float e[4] = {c4[x].x, c4[x].y, c4[x].z, c4[x].w};
+#pragma unroll
+                    for (int y = 0; y < 4; y++) {
+                        const double v = (double)e[y];
+                        cnt += (ci + y < cend && (sh ? v <= thr : v < thr)) ? 1 : 0;
+                    }
+                }
+            }
+            cnt += __shfl_xor_sync(FULL, cnt, 1);
+            cnt += __shfl_xor_sync(FULL, cnt, 2);
+            b = b1 > 0 ? cb + cnt : 0;
+        }
+        {
+            const int64_t blk = (int64_t)max(b - 1, 0) * COARSE;  // 64 row values [blk, blk + 64)
+            int cnt = 0;
+            if (act) {
+                const float *rr = P.sdist + (int64_t)a * n + blk;
+                float4 r4[4];
+#pragma unroll
+                for (int x = 0; x < 4; x++) r4[x] = __ldg(reinterpret_cast<const float4 *>(rr + sl * 16) + x);
+#pragma unroll
+                for (int x = 0; x < 4; x++) {
+                    const float e[4] = {r4[x].x, r4[x].y, r4[x].z, r4[x].w};
+#pragma unroll
+                    for (int y = 0; y < 4; y++) {
+                        const double v = (double)e[y];
+                        cnt += (sh ? v <= thr : v < thr) ? 1 : 0;
+                    }
+                }
+            }
+            cnt += __shfl_xor_sync(FULL, cnt, 1);
+            cnt += __shfl_xor_sync(FULL, cnt, 2);
+            res = (int)(blk + cnt);
+        }
+    } else {
     int b;
     {
         const int b1 = sh ? b1hi : b1lo;
@@ -895,7 +970,6 @@ __device__ __forceinline__ double dist_window8(const BulkParams &P, int a, const
         b = b1 > 0 ? cb + 1 + cnt : 0;
     }
     // fine round: <= 63 row values
-    int res;
     {
         const int64_t s0 = b > 0 ? (int64_t)(b - 1) * COARSE + 1 : 0;
         const int64_t s1 = b < nb ? (int64_t)b * COARSE : n;
@@ -914,6 +988,7 @@ __device__ __forceinline__ double dist_window8(const BulkParams &P, int a, const
         cnt += __shfl_xor_sync(FULL, cnt, 1);
         cnt += __shfl_xor_sync(FULL, cnt, 2);
         res = (int)(s0 + cnt);
+    }
     }
     wlo = __shfl_sync(FULL, res, gb);
     whi = __shfl_sync(FULL, res, gb | 4);
@@ -1075,13 +1150,23 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
                 const int tot = __shfl_sync(FULL, inc, gb | 7);
                 const int ex = run + inc - c;
                 if (apos < 0 && kk >= ex && kk < ex + c) {
-                    int kr = kk - ex;
+                    int kr = kk - ex, xs = 0, ks = 0;
+                    uint32_t ws = 0;
 #pragma unroll
                     for (int x = 0; x < 4; x++) {
                         const int cx = __popc(wd[x]);
-                        if (kr >= 0 && kr < cx) apos = (w0 + x) * 32 + (int)__fns(wd[x], 0u, kr + 1);
+                        if (kr >= 0 && kr < cx) {
+                            ws = wd[x];
+                            xs = x;
+                            ks = kr;
+                        }
                         kr -= cx;
                     }
+#ifdef RIANN_DRAW_FNS
+                    apos = (w0 + xs) * 32 + (int)__fns(ws, 0u, ks + 1);
+#else
+                    apos = (w0 + xs) * 32 + nth_bit(ws, ks);
+#endif
                 }
                 run += tot;
             }

@@ -356,19 +356,26 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
             lenB8 = (cS - cA + 7) & ~7;
             gap = lenA8 - cA;
             __syncwarp();
-            // enumerate ascending into the slot, clearing the bitmap; rank and presence of p.
-            // Step t: lane L takes words 128t + 4L .. +3 (one LDS.128); one warp scan per step.
+            // enumerate ascending; rank and presence of p.  Step t: lane L takes words
+            // 128t + 4L .. +3 (one LDS.128); one warp scan per step.  The list is staged
+            // in place: the entries of steps 0 .. t fit in the bitmap words those steps
+            // have consumed as long as the list holds <= 1 entry per 16 bits so far
+            // (positions run .. of a denser window go straight to the slot from then
+            // on), and is copied out with 16-byte stores.
             uint16_t *slot = P.pool + off;
+            uint16_t *stg = reinterpret_cast<uint16_t *>(bm);
             const int wp = p >> 5;
             int run = 0;
+            bool stage_ok = true;
+            int fin = 0;  // list positions [0, fin) are staged
             for (int t = 0; t < NW; t += 128) {
                 const int w0 = t + 4 * lane;
-                uint4 q4 = *reinterpret_cast<const uint4 *>(bm + w0);
+                const uint4 q4 = *reinterpret_cast<const uint4 *>(bm + w0);
                 const uint32_t any4 = q4.x | q4.y | q4.z | q4.w;
                 if (!__any_sync(FULL, any4 != 0u)) continue;
-                if (any4) *reinterpret_cast<uint4 *>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
                 const int c = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
                 const int inc = warp_incl_scan(c, lane);
+                const int tot = __shfl_sync(FULL, inc, 31);
                 int o = run + inc - c;
                 if ((wp >> 2) == (w0 >> 2)) {  // this lane holds p's word
                     const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
@@ -377,13 +384,15 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                     below = bb + __popc(wd[wp & 3] & ((1u << (p & 31)) - 1u));
                     p_in = (wd[wp & 3] >> (p & 31)) & 1u;
                 }
-                if (any4) {
+                stage_ok = stage_ok && 2 * (run + tot + 7) <= 4 * (t + 128);
+                __syncwarp();  // every lane holds its words: the staged list may grow over them
+                auto emit = [&](uint16_t *out) {
                     bool crossed = w0 * 32 >= jh;
-                    uint16_t *dst = slot + o + (crossed ? gap : 0);
+                    uint16_t *dst = out + o + (crossed ? gap : 0);
                     const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
                     if ((jh & 31) == 0) {
                         // part boundary on a word boundary: one check per word
-    #pragma unroll
+#pragma unroll
                         for (int k = 0; k < 4; k++) {
                             uint32_t word = wd[k];
                             const uint32_t base = (uint32_t)(w0 + k) * 32u;
@@ -397,7 +406,7 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                             }
                         }
                     } else {
-    #pragma unroll
+#pragma unroll
                         for (int k = 0; k < 4; k++) {
                             uint32_t word = wd[k];
                             const uint32_t base = (uint32_t)(w0 + k) * 32u;
@@ -413,9 +422,25 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                             }
                         }
                     }
+                };
+                if (any4) {
+                    if (stage_ok) emit(stg);
+                    else emit(slot);
                 }
-                run += __shfl_sync(FULL, inc, 31);
+                run += tot;
+                if (stage_ok) fin = run <= cA ? run : run + gap;
             }
+            __syncwarp();
+            {
+                // staged positions [0, fin): whole 16-byte groups, then the tail
+                const int nv = fin >> 3;
+                for (int i = lane; i < nv; i += 32)
+                    reinterpret_cast<uint4 *>(slot)[i] = reinterpret_cast<const uint4 *>(stg)[i];
+                if (lane < (fin & 7)) slot[8 * nv + lane] = stg[8 * nv + lane];
+            }
+            __syncwarp();
+            for (int w = lane * 4; w < NW; w += 128) *reinterpret_cast<uint4 *>(bm + w) = make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
             const int lp = (wp >> 2) & 31;
             below = __shfl_sync(FULL, below, lp);
             p_in = __shfl_sync(FULL, p_in, lp);

@@ -201,7 +201,7 @@ __host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 4095)
 // per-warp shared words: the n-bit bitmap, at least 8 KB (the radix path's buffers)
 __host__ __device__ constexpr int p0_smem_words(int64_t n) { return p0_words(n) > 2048 ? p0_words(n) : 2048; }
 #ifndef RIANN_P0_RADIX_CAP
-#define RIANN_P0_RADIX_CAP 1024
+#define RIANN_P0_RADIX_CAP 512
 #endif
 constexpr int P0_RADIX_CAP = RIANN_P0_RADIX_CAP;  // windows up to this many entries take the radix path
 

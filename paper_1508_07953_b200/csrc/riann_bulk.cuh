@@ -358,16 +358,26 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
             __syncwarp();
             // enumerate ascending; rank and presence of p.  Step t: lane L takes words
             // 128t + 4L .. +3 (one LDS.128); one warp scan per step.  The list is staged
-            // in place: the entries of steps 0 .. t fit in the bitmap words those steps
-            // have consumed as long as the list holds <= 1 entry per 16 bits so far
-            // (positions run .. of a denser window go straight to the slot from then
-            // on), and is copied out with 16-byte stores.
+            // in place, over the bitmap words the steps so far have consumed (a denser
+            // window flushes and restarts the staging area; a step that still does not
+            // fit goes straight to the slot), and copied out with 16-byte stores.
             uint16_t *slot = P.pool + off;
             uint16_t *stg = reinterpret_cast<uint16_t *>(bm);
             const int wp = p >> 5;
             int run = 0;
-            bool stage_ok = true;
-            int fin = 0;  // list positions [0, fin) are staged
+            // list positions [spos, fin) are staged at stg[pos - sbase] (sbase = spos & ~7)
+            int spos = 0, fin = 0, sbase = 0;
+            auto flush = [&]() {
+                __syncwarp();
+                const int a8 = min(fin, (spos + 7) & ~7);
+                if (spos + lane < a8) slot[spos + lane] = stg[spos + lane - sbase];
+                const int nv = (fin - a8) >> 3;
+                for (int i = lane; i < nv; i += 32)
+                    reinterpret_cast<uint4 *>(slot + a8)[i] = reinterpret_cast<const uint4 *>(stg + (a8 - sbase))[i];
+                const int tp = a8 + 8 * nv;
+                if (tp + lane < fin) slot[tp + lane] = stg[tp + lane - sbase];
+                __syncwarp();
+            };
             for (int t = 0; t < NW; t += 128) {
                 const int w0 = t + 4 * lane;
                 const uint4 q4 = *reinterpret_cast<const uint4 *>(bm + w0);
@@ -384,7 +394,17 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                     below = bb + __popc(wd[wp & 3] & ((1u << (p & 31)) - 1u));
                     p_in = (wd[wp & 3] >> (p & 31)) & 1u;
                 }
-                stage_ok = stage_ok && 2 * (run + tot + 7) <= 4 * (t + 128);
+                // the step's entries end before position run + tot + 7; 2 (t + 128) entries
+                // fit in the words consumed so far.  A denser window flushes what is
+                // staged and restarts the staging area at this step's first position.
+                const int posb = run < cA ? run : run + gap;
+                bool stage_ok = run + tot + 7 - sbase <= 2 * (t + 128);
+                if (!stage_ok) {
+                    if (fin > spos) flush();
+                    spos = fin = posb;
+                    sbase = spos & ~7;
+                    stage_ok = run + tot + 7 - sbase <= 2 * (t + 128);
+                }
                 __syncwarp();  // every lane holds its words: the staged list may grow over them
                 auto emit = [&](uint16_t *out) {
                     bool crossed = w0 * 32 >= jh;
@@ -424,20 +444,17 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                     }
                 };
                 if (any4) {
-                    if (stage_ok) emit(stg);
+                    if (stage_ok) emit(stg - sbase);
                     else emit(slot);
                 }
                 run += tot;
-                if (stage_ok) fin = run <= cA ? run : run + gap;
+                fin = run <= cA ? run : run + gap;
+                if (!stage_ok) {  // written straight to the slot: nothing staged
+                    spos = fin;
+                    sbase = spos & ~7;
+                }
             }
-            __syncwarp();
-            {
-                // staged positions [0, fin): whole 16-byte groups, then the tail
-                const int nv = fin >> 3;
-                for (int i = lane; i < nv; i += 32)
-                    reinterpret_cast<uint4 *>(slot)[i] = reinterpret_cast<const uint4 *>(stg)[i];
-                if (lane < (fin & 7)) slot[8 * nv + lane] = stg[8 * nv + lane];
-            }
+            if (fin > spos) flush();
             __syncwarp();
             for (int w = lane * 4; w < NW; w += 128) *reinterpret_cast<uint4 *>(bm + w) = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();

@@ -1073,15 +1073,26 @@ __global__ void __launch_bounds__(256, RIANN_P0A_MINB) bulk_p0a_kernel(BulkParam
         load_qv8<D>(P.units + g * D, qv, gl);
         int lo, hi;
         const double d = dist_window8<D>(P, ok ? p : 0, qv, ok, gl, gb, lo, hi);
-        if (ok && gl == 0) {
-            QState *sp = P.st + g;
-            const int cS = hi - lo;
-            const int alloc = (cS + 14 + 127) & ~127;  // >= lenA8 + lenB8; bits of a list 16-byte aligned
-            int64_t off = -1;
-            if (cS <= LIGHT_MAX) {
-                off = (int64_t)atomicAdd(P.pool_top, (unsigned long long)alloc);
+        // list allocation: one atomic per warp for its (up to four) queries
+        const int cS = hi - lo;
+        const int alloc = (cS + 14 + 127) & ~127;  // >= lenA8 + lenB8; bits of a list 16-byte aligned
+        int64_t off = -1;
+        {
+            const int want = (ok && gl == 0 && cS <= LIGHT_MAX) ? alloc : 0;
+            int inc = want;  // inclusive sum over the group leaders (lanes 0, 8, 16, 24)
+            inc += __shfl_up_sync(FULL, inc, 8) * (lane >= 8 ? 1 : 0);
+            inc += __shfl_up_sync(FULL, inc, 16) * (lane >= 16 ? 1 : 0);
+            const int tot = __shfl_sync(FULL, inc, 24);
+            unsigned long long base = 0;
+            if (lane == 0 && tot > 0) base = atomicAdd(P.pool_top, (unsigned long long)tot);
+            base = __shfl_sync(FULL, base, 0);
+            if (want > 0) {
+                off = (int64_t)base + (inc - want);
                 if (off + alloc > P.pool_cap) off = -1;
             }
+        }
+        if (ok && gl == 0) {
+            QState *sp = P.st + g;
             RB_CHECK(lo >= 0 && lo <= hi && hi <= P.n, 1);
             RB_CHECK(off < 0 || off + alloc <= P.pool_cap, 2);
             sp->d_prev = d;
@@ -1224,6 +1235,11 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
             RB_CHECK(an >= 0 && an < P.n && nu < BULK_U, 31);
         }
         an = __shfl_sync(FULL, an, gb);
+        // active list slots: one atomic per warp for its (up to four) drawing queries
+        const unsigned act_m = __ballot_sync(FULL, has && gl == 0 && drew);
+        int act_base = 0;
+        if (lane == 0 && act_m) act_base = atomicAdd(P.n_active_out, __popc(act_m));
+        act_base = __shfl_sync(FULL, act_base, 0);
         if (has && gl == 0) {
             sp->tests += cS;
             sp->rings = rings;
@@ -1240,7 +1256,7 @@ __global__ void __launch_bounds__(256, RIANN_DRAW_MINB) bulk_draw_kernel(BulkPar
                 sp->nu = nu + 1;
                 rng_store(*sp, rng);
                 status = ST_ACTIVE;
-                P.active_out[atomicAdd(P.n_active_out, 1)] = (int32_t)g;
+                P.active_out[act_base + __popc(act_m & lanemask_lt())] = (int32_t)g;
                 atomicAdd(P.counts + an, 1);  // grouping by anchor for the next phase
             } else if (want) {
                 status = ST_HEAVY;

@@ -362,7 +362,11 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
             // window flushes and restarts the staging area; a step that still does not
             // fit goes straight to the slot), and copied out with 16-byte stores.
             uint16_t *slot = P.pool + off;
-            uint16_t *stg = reinterpret_cast<uint16_t *>(bm);
+            // small n: the bitmap leaves at least half of the warp's 8 KB free; the list
+            // is staged there (fixed capacity) instead of over the consumed words
+            const bool tail_stage = NW <= 1024;
+            const int tail_cap = 2 * (p0_smem_words(n) - NW);  // entries
+            uint16_t *stg = reinterpret_cast<uint16_t *>(tail_stage ? bm + NW : bm);
             const int wp = p >> 5;
             int run = 0;
             // list positions [spos, fin) are staged at stg[pos - sbase] (sbase = spos & ~7)
@@ -398,12 +402,13 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                 // fit in the words consumed so far.  A denser window flushes what is
                 // staged and restarts the staging area at this step's first position.
                 const int posb = run < cA ? run : run + gap;
-                bool stage_ok = run + tot + 7 - sbase <= 2 * (t + 128);
+                const int cap_t = tail_stage ? tail_cap : 2 * (t + 128);
+                bool stage_ok = run + tot + 7 - sbase <= cap_t;
                 if (!stage_ok) {
                     if (fin > spos) flush();
                     spos = fin = posb;
                     sbase = spos & ~7;
-                    stage_ok = run + tot + 7 - sbase <= 2 * (t + 128);
+                    stage_ok = run + tot + 7 - sbase <= cap_t;
                 }
                 __syncwarp();  // every lane holds its words: the staged list may grow over them
                 auto emit = [&](uint16_t *out) {
@@ -456,7 +461,8 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
             }
             if (fin > spos) flush();
             __syncwarp();
-            for (int w = lane * 4; w < NW; w += 128) *reinterpret_cast<uint4 *>(bm + w) = make_uint4(0u, 0u, 0u, 0u);
+            // the bitmap and the radix path's cursors (words 0 .. 255) are zero between queries
+            for (int w = lane * 4; w < max(NW, 256); w += 128) *reinterpret_cast<uint4 *>(bm + w) = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();
             const int lp = (wp >> 2) & 31;
             below = __shfl_sync(FULL, below, lp);

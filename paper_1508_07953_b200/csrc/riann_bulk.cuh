@@ -200,6 +200,10 @@ __device__ __forceinline__ int bit_at(const uint8_t *bits, int64_t e) { return (
 __host__ __device__ constexpr int p0_words(int64_t n) { return (int)(((n + 4095) / 4096) * 128); }
 // per-warp shared words: the n-bit bitmap, at least 8 KB (the radix path's buffers)
 __host__ __device__ constexpr int p0_smem_words(int64_t n) { return p0_words(n) > 2048 ? p0_words(n) : 2048; }
+#ifndef RIANN_P0_DENSE_STEP
+#define RIANN_P0_DENSE_STEP 2048
+#endif
+constexpr int P0_DENSE_STEP = RIANN_P0_DENSE_STEP;  // entries per 4,096-bit step from which unstaged steps go word by word
 #ifndef RIANN_P0_RADIX_CAP
 #define RIANN_P0_RADIX_CAP 512
 #endif
@@ -448,9 +452,29 @@ __global__ void __launch_bounds__(RIANN_P0_WPB * 32, 24 / RIANN_P0_WPB) bulk_p0_
                         }
                     }
                 };
-                if (any4) {
-                    if (stage_ok) emit(stg - sbase);
-                    else emit(slot);
+                if (stage_ok) {
+                    if (any4) emit(stg - sbase);
+                } else if (tot < P0_DENSE_STEP) {
+                    if (any4) emit(slot);
+                } else {
+                    // a step too dense to stage (>= 1 entry per 16 bits so far): word by
+                    // word, lane b takes bit b, so the set bits of a word go to consecutive
+                    // list positions with one coalesced store
+                    for (int ls = 0; ls < 32; ls++) {
+                        const uint32_t wx = __shfl_sync(FULL, q4.x, ls), wy = __shfl_sync(FULL, q4.y, ls);
+                        const uint32_t wz = __shfl_sync(FULL, q4.z, ls), ww = __shfl_sync(FULL, q4.w, ls);
+                        int ob = __shfl_sync(FULL, o, ls);
+                        if ((wx | wy | wz | ww) == 0u) continue;  // warp-uniform
+                        const uint32_t wd[4] = {wx, wy, wz, ww};
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            const uint32_t word = wd[k];
+                            const int j = (t + 4 * ls + k) * 32 + lane;
+                            if ((word >> lane) & 1u)
+                                slot[ob + __popc(word & lanemask_lt()) + (j >= jh ? gap : 0)] = (uint16_t)j;
+                            ob += __popc(word);
+                        }
+                    }
                 }
                 run += tot;
                 fin = run <= cA ? run : run + gap;

@@ -165,8 +165,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// the registers of a tmem_ld32 are valid only after the next tmem_ld_wait
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                                                                const __grid_constant__ CUtensorMap mapB, ExactParams P)
@@ -304,10 +305,13 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
             }
             bar_wait(&acc_full[acc], (unsigned)((t / 2) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-            for (int k = 0; k < HALF / 32; k++) {
-                uint32_t acc32[32];
-                tmem_ld32(tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN + h * HALF + k * 32), acc32);
+            // the TMEM load of column block k + 1 is in flight while block k is screened
+            // (tcgen05.wait::ld covers every load issued before it, so the wait for
+            // block k comes before block k + 1 is issued)
+            const uint32_t tcol = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN + h * HALF);
+            uint32_t accA[32], accB[32];
+            tmem_ld32(tcol, accA);
+            auto screen = [&](const int k, const uint32_t (&acc32)[32]) {
                 // fast path: w = (1+E)nr - acc; u2 = cu + w is an upper bound of d^2
                 float wmin = inf;
 #pragma unroll
@@ -358,6 +362,15 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
                         cnt++;
                     }
                 }
+            };
+#pragma unroll
+            for (int k = 0; k < HALF / 32; k += 2) {
+                tmem_ld_wait();
+                tmem_ld32(tcol + (uint32_t)((k + 1) * 32), accB);
+                screen(k, accA);
+                tmem_ld_wait();
+                if (k + 2 < HALF / 32) tmem_ld32(tcol + (uint32_t)((k + 2) * 32), accA);
+                screen(k + 1, accB);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();

@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
                     const uint64_t da = smem_desc(sA + k * A_BLOCK), db = smem_desc(sB + s * STAGE_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; kk++)  // 16 fp16 = 32 bytes per MMA step
+#ifdef RIANN_K4_NOMMA  // timing probe: the epilogue alone (results are garbage)
+                        if (P.n < 0)
+#endif
                         mma_f16(tacc, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc, (k | kk) ? 1u : 0u);
                     mma_commit(&empty_bar[s]);
                     if (k == kb - 1) mma_commit(&acc_full[acc]);
@@ -365,6 +368,9 @@ __global__ void __launch_bounds__(THREADS, 1) exact_tc_kernel(const __grid_const
             };
 #pragma unroll
             for (int k = 0; k < HALF / 32; k += 2) {
+#ifdef RIANN_K4_NOEPI  // timing probe: the MMA pipeline alone (results are garbage)
+                if (P.n > 0) break;
+#endif
                 tmem_ld_wait();
                 tmem_ld32(tcol + (uint32_t)((k + 1) * 32), accB);
                 screen(k, accA);

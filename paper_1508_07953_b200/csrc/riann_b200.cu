@@ -582,6 +582,15 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
             CK(cudaMemsetAsync(ctr + out, 0, 4, c->stream));
             CK(cudaMemsetAsync(ctr + 3, 0, 4, c->stream));
             tmark(c, PH_GROUP);
+#ifndef RIANN_COMPACT
+#define RIANN_COMPACT 1
+#endif
+            if (RIANN_COMPACT && ph >= 1) {
+                // dense lists (mostly dead by now) are rewritten before the phases left read them again
+                rb::bulk_compact_kernel<<<(unsigned)c->sms * 8, 256, 0, c->stream>>>(B, phases - ph);
+                CK(cudaGetLastError());
+                c->launches += 1;
+            }
             rb::anchor_scan_kernel<<<1, rb::SCAN_T, 0, c->stream>>>(B.counts, B.starts, (int)(n + 1));
             CK(cudaGetLastError());
             rb::bulk_scatter_kernel<<<small_grid, 256, 0, c->stream>>>(B);

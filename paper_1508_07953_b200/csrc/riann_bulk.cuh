@@ -557,6 +557,148 @@ __global__ void bulk_scatter_kernel(BulkParams P)
 }
 
 // ---------------------------------------------------------------------------
+// List compaction between ring phases (dense first rings: a stream's first
+// frame, high-motion clips).  The fixed lists keep their dead entries, so every
+// filter phase and the final scan pay for the first ring's size; once the dead
+// entries of a query, times the filter phases left, outweigh one rewrite, the
+// warp rewrites the list in place (ascending order kept, parts A / B
+// compacted separately, padding as in P0b), sets the alive bits of the new
+// layout and remaps the list positions the state holds (used anchors still in
+// S, prev).  S itself does not change, so results are unaffected.
+#ifndef RIANN_COMPACT_X2
+#define RIANN_COMPACT_X2 3  // compact when 2 (W - |S|) phases_left >= RIANN_COMPACT_X2 W
+#endif
+__global__ void __launch_bounds__(256) bulk_compact_kernel(BulkParams P, int phases_left)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int m = *P.n_active_in;
+    const int jh = (int)(P.n >> 1);
+    constexpr int CK = 4;
+    __shared__ __align__(16) uint16_t stg_all[8][256 * CK + 16];
+    uint16_t *stg = stg_all[threadIdx.x >> 5];
+    for (int64_t ib = gwarp * 32; ib < m; ib += nwarps * 32) {
+        // criterion, a lane per query
+        int gq = -1;
+        if (ib + lane < m) {
+            const int g = P.active_in[ib + lane];
+            const QState &s = P.st[g];
+            const int W = s.lenA8 + s.lenB8;
+            if (W >= 256 && 2ll * (W - s.cS) * phases_left >= (long long)RIANN_COMPACT_X2 * W) gq = g;
+        }
+        unsigned todo = __ballot_sync(FULL, gq >= 0);
+        while (todo) {
+            const int l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int g = __shfl_sync(FULL, gq, l);
+            QState *sp = P.st + g;
+            const int64_t soff = sp->s_off;
+            const int lenA8 = sp->lenA8, lenB8 = sp->lenB8, nu = sp->nu, pin = sp->pin_pos;
+            uint16_t *slot = P.pool + soff;
+            uint8_t *bs = (sp->sel ? P.bits1 : P.bits0) + (soff >> 3);  // the buffer holding S
+            uint8_t *bo = (sp->sel ? P.bits0 : P.bits1) + (soff >> 3);  // the next filter's output
+            // tracked list positions: lanes 0 .. nu - 1 the used anchors, lane nu prev
+            int tpos = -1;
+            if (lane < nu) tpos = sp->up[lane];
+            else if (lane == nu) tpos = pin;
+            int tval = -1;
+            if (tpos >= 0 && ((bs[tpos >> 3] >> (tpos & 7)) & 1)) tval = slot[tpos];  // alive: its reference index
+            __syncwarp();
+            // compact one part: entries [r0, r0 + len8) -> from position w0; returns the
+            // count.  CK chunks of 256 entries are loaded before any is written (the
+            // output never passes the input), the survivors staged in shared memory
+            // and copied out with 16-byte stores.
+            auto part = [&](int r0, int len8, int w0) {
+                int out = w0;
+                for (int e0 = 0; e0 < len8; e0 += 256 * CK) {
+                    uint4 v[CK];
+                    uint32_t al[CK];
+#pragma unroll
+                    for (int u = 0; u < CK; u++) {
+                        const int e = e0 + (u * 32 + lane) * 8;
+                        v[u] = make_uint4(0u, 0u, 0u, 0u);
+                        al[u] = 0;
+                        if (e < len8) {
+                            v[u] = *reinterpret_cast<const uint4 *>(slot + r0 + e);
+                            al[u] = bs[(r0 + e) >> 3];
+                        }
+                    }
+                    const int sbase = out & ~7;
+                    int fin = out;
+#pragma unroll
+                    for (int u = 0; u < CK; u++) {
+                        const int c = __popc(al[u]);
+                        const int inc = warp_incl_scan(c, lane);
+                        int o = fin + inc - c - sbase;
+                        const uint16_t *e8 = reinterpret_cast<const uint16_t *>(&v[u]);
+#pragma unroll
+                        for (int x = 0; x < 8; x++)
+                            if ((al[u] >> x) & 1u) stg[o++] = e8[x];
+                        fin += __shfl_sync(FULL, inc, 31);
+                    }
+                    __syncwarp();
+                    // list positions [out, fin) are staged at stg[pos - sbase]
+                    const int a8 = min(fin, (out + 7) & ~7);
+                    if (out + lane < a8) slot[out + lane] = stg[out + lane - sbase];
+                    const int nv = (fin - a8) >> 3;
+                    for (int i = lane; i < nv; i += 32)
+                        reinterpret_cast<uint4 *>(slot + a8)[i] = reinterpret_cast<const uint4 *>(stg + (a8 - sbase))[i];
+                    const int tp = a8 + 8 * nv;
+                    if (tp + lane < fin) slot[tp + lane] = stg[tp + lane - sbase];
+                    out = fin;
+                    __syncwarp();
+                }
+                return out - w0;
+            };
+            const int cA = part(0, lenA8, 0);
+            const int nA8 = (cA + 7) & ~7;
+            if (cA + lane < nA8) slot[cA + lane] = 0;  // padding: valid indices of the part (P0b)
+            __syncwarp();
+            const int cB = part(lenA8, lenB8, nA8);
+            const int nB8 = (cB + 7) & ~7;
+            if (nA8 + cB + lane < nA8 + nB8) slot[nA8 + cB + lane] = (uint16_t)jh;
+            // alive bits of the new layout in both buffers, zero up to the old end (whole
+            // words: lists are allocated in multiples of 128 entries)
+            {
+                auto below = [](int x) { return x <= 0 ? 0u : x >= 32 ? 0xffffffffu : (1u << x) - 1u; };
+                const int nwo = (lenA8 + lenB8 + 31) >> 5;
+                uint32_t *ws = reinterpret_cast<uint32_t *>(bs), *wo = reinterpret_cast<uint32_t *>(bo);
+                for (int w = lane; w < nwo; w += 32) {
+                    const int i0 = 32 * w;
+                    ws[w] = below(cA - i0) | (below(nA8 + cB - i0) & ~below(nA8 - i0));
+                    wo[w] = 0u;
+                }
+            }
+            __syncwarp();
+            // new positions of the tracked entries: binary search of the index in its part
+            int npos = -1;
+            if (tval >= 0) {
+                int lo = tval < jh ? 0 : nA8, hi = tval < jh ? cA : nA8 + cB;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if ((int)slot[mid] < tval) lo = mid + 1;
+                    else hi = mid;
+                }
+                npos = lo;
+                RB_CHECK(lo < nA8 + cB && (int)slot[lo] == tval, 60);
+            }
+            const unsigned keepm = __ballot_sync(FULL, lane < nu && npos >= 0);
+            if (lane < nu && npos >= 0) sp->up[__popc(keepm & lanemask_lt())] = (uint16_t)npos;
+            const int npin = __shfl_sync(FULL, npos, nu & 31);
+            if (lane == 0) {
+                sp->nu = __popc(keepm);
+                sp->pin_pos = pin >= 0 ? npin : -1;
+                sp->lenA8 = nA8;
+                sp->lenB8 = nB8;
+                RB_CHECK(cA + cB == sp->cS && nA8 <= lenA8 && nA8 + nB8 <= lenA8 + lenB8, 61);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void *p)
 {
     return (uint32_t)__cvta_generic_to_shared(p);

@@ -486,7 +486,7 @@ def run_ncu_child(a):
 def kernel_group(name):
     for key, label in (("units_warp", "units"), ("units_tile", "units"), ("units_kernel", "units"), ("pw_tree", "tc_tree"),
                        ("proj_kernel", "projection"), ("bulk_p0a", "p0a"), ("bulk_p0_", "p0b"),
-                       ("bulk_draw", "draw"), ("anchor_scan", "group"), ("bulk_scatter", "group"),
+                       ("bulk_draw", "draw"), ("anchor_scan", "group"), ("bulk_scatter", "group"), ("bulk_compact", "group"),
                        ("bulk_window", "window"), ("bulk_filter", "filter"), ("bulk_final", "final"),
                        ("query_kernel", "query (K2)")):
         if key in name:

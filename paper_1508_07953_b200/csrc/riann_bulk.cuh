@@ -568,14 +568,20 @@ __global__ void bulk_scatter_kernel(BulkParams P)
 #ifndef RIANN_COMPACT_X2
 #define RIANN_COMPACT_X2 3  // compact when 2 (W - |S|) phases_left >= RIANN_COMPACT_X2 W
 #endif
-__global__ void __launch_bounds__(256) bulk_compact_kernel(BulkParams P, int phases_left)
+#ifndef RIANN_COMPACT_CK
+#define RIANN_COMPACT_CK 4  // chunks of 256 entries loaded per step
+#endif
+#ifndef RIANN_COMPACT_MINB
+#define RIANN_COMPACT_MINB 4
+#endif
+__global__ void __launch_bounds__(256, RIANN_COMPACT_MINB) bulk_compact_kernel(BulkParams P, int phases_left)
 {
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int m = *P.n_active_in;
     const int jh = (int)(P.n >> 1);
-    constexpr int CK = 4;
+    constexpr int CK = RIANN_COMPACT_CK;
     __shared__ __align__(16) uint16_t stg_all[8][256 * CK + 16];
     uint16_t *stg = stg_all[threadIdx.x >> 5];
     for (int64_t ib = gwarp * 32; ib < m; ib += nwarps * 32) {

@@ -105,6 +105,34 @@ def test_cfg3_full_scale_vs_oracle(R, oracle_mod):
         prev = r["idx"]
 
 
+@pytest.mark.parametrize("L,alpha,max_rings", [(20, 0.25, 8), (2, 0.4, 14), (40, 0.15, 20)])
+def test_dense_lists_compaction_vs_oracle(R, oracle_mod, L, alpha, max_rings):
+    """Dense first rings (config 2: high motion, first rings ~60 % of n; frame 1
+    from init_field: ~70 %): the lists are rewritten between ring phases
+    (bulk_compact_kernel), several times with long ring caps.  8,192
+    stratified positions through 4 frames, bit-exact vs the oracle."""
+    from paper_1508_07953_b200 import workloads as W
+
+    cfg = W.CONFIGS[2]
+    T = 4
+    frames = list(W.iter_clip(cfg, T))
+    refs = W.reference_set(cfg)
+    model = R.ReferenceModel.from_refs(refs, cfg.patch, channels=cfg.channels)
+    gw, gh = cfg.grid
+    pos = _stratified(gw, gh, 8192, 35)
+    params = R.SearchParams(L=L, alpha=alpha, max_rings=max_rings)
+    gpu = [(fld.indices.ravel()[pos].copy(), fld.distances.ravel()[pos].copy())
+           for _, fld, _ in R.stream_fields(model, frames, params)]
+    om = oracle_mod.LazyOracleModel(refs)
+    prev = oracle_mod.init_field_indices(gw, gh, cfg.n_refs, 0).ravel()[pos]
+    for t in range(T):
+        unit = oracle_mod.normalize_rows(W.patch_rows(frames[t], cfg.patch, pos // gw, pos % gw))[0]
+        r = oracle_mod.query_positions(om, unit, prev, pos, gw, 0, t + 1, L=L, alpha=alpha, max_rings=max_rings)
+        assert np.array_equal(gpu[t][0], r["idx"]), t
+        assert np.array_equal(_bits(gpu[t][1]), _bits(r["dist"])), t
+        prev = r["idx"]
+
+
 def test_cfg3_full_scale_rings_evals(R, oracle_mod):
     """Same workload through riann_query_batch (the per-query kernel on the
     same model): rings, evals and |S| per position equal the oracle's."""

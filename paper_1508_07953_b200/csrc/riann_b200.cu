@@ -585,7 +585,8 @@ int run_bulk_t(riann_ctx *c, rb::QueryParams &Pq)
 #ifndef RIANN_COMPACT
 #define RIANN_COMPACT 1
 #endif
-            if (RIANN_COMPACT && ph >= 1 && QN >= 16384) {  // tiny frames are launch-bound: skip
+            // tiny frames are launch-bound: skip; with one phase left the criterion cannot hold
+            if (RIANN_COMPACT && ph >= 1 && QN >= 16384 && 2 * (phases - ph) > RIANN_COMPACT_X2) {
                 // dense lists (mostly dead by now) are rewritten before the phases left read them again
                 rb::bulk_compact_kernel<<<(unsigned)c->sms * 8, 256, 0, c->stream>>>(B, phases - ph);
                 CK(cudaGetLastError());

@@ -1891,6 +1891,7 @@ __global__ void refs_pca_kernel(const float *refs, const float *T, int64_t n, in
 // the run totals.  Replaces a library scan + memset (two launches) per ring
 // phase.
 constexpr int SCAN_T = 1024;
+constexpr int SCAN_E = 68;  // counts per thread of the one-pass scan: 1,024 x 68 >= 65,536 + 1
 __global__ void __launch_bounds__(SCAN_T) anchor_scan_kernel(int32_t *counts, int32_t *starts, int m)
 {
     __shared__ int32_t wsum[SCAN_T / 32];
@@ -1898,6 +1899,72 @@ __global__ void __launch_bounds__(SCAN_T) anchor_scan_kernel(int32_t *counts, in
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) carry_s = 0;
     __syncthreads();
+    // m <= SCAN_T * SCAN_E (every bulk-path n): a thread owns `per` contiguous counts
+    // (a multiple of 4): one round of independent loads for the thread sums, one
+    // block scan, a second round (cache hits) for the prefix and the stores
+    if (m <= SCAN_T * SCAN_E) {
+        const int per = (((m + SCAN_T - 1) / SCAN_T) + 3) & ~3;
+        const int i0 = tid * per;
+        auto ld4 = [&](int i) {
+            int4 v = make_int4(0, 0, 0, 0);
+            if (i + 3 < m) {
+                v = *reinterpret_cast<const int4 *>(counts + i);
+            } else if (i < m) {
+                v.x = counts[i];
+                if (i + 1 < m) v.y = counts[i + 1];
+                if (i + 2 < m) v.z = counts[i + 2];
+            }
+            return v;
+        };
+        int tsum = 0;
+#pragma unroll 17
+        for (int k = 0; k < per; k += 4) {
+            const int4 v = ld4(i0 + k);
+            tsum += v.x + v.y + v.z + v.w;
+        }
+        int inc = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const int x = wsum[lane];
+            int xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += y;
+            }
+            wsum[lane] = xi - x;  // exclusive warp offsets
+        }
+        __syncthreads();
+        int run = wsum[w] + inc - tsum;
+#pragma unroll 4
+        for (int k = 0; k < per; k += 4) {
+            const int i = i0 + k;
+            if (i >= m) break;
+            const int4 v = ld4(i);
+            int4 o4;
+            o4.x = run;
+            o4.y = o4.x + v.x;
+            o4.z = o4.y + v.y;
+            o4.w = o4.z + v.z;
+            run = o4.w + v.w;
+            if (i + 3 < m) {
+                *reinterpret_cast<int4 *>(starts + i) = o4;
+                *reinterpret_cast<int4 *>(counts + i) = make_int4(0, 0, 0, 0);
+            } else {
+                starts[i] = o4.x;
+                counts[i] = 0;
+                if (i + 1 < m) { starts[i + 1] = o4.y; counts[i + 1] = 0; }
+                if (i + 2 < m) { starts[i + 2] = o4.z; counts[i + 2] = 0; }
+            }
+        }
+        return;
+    }
     // tiles of SCAN_T * 4 elements, int4-coalesced per thread
     for (int base = 0; base < m; base += SCAN_T * 4) {
         int v[4];

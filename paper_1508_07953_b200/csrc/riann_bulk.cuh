@@ -1499,18 +1499,10 @@ __global__ void __launch_bounds__(256, RIANN_WIN_MINB) bulk_window_kernel(BulkPa
 #ifndef RIANN_PCA_CHUNKMAJOR
 #define RIANN_PCA_CHUNKMAJOR 1
 #endif
-// RIANN_FINAL_C0 = 2: chunks 0 and 1 of a reference form one 64-byte record
-// (one L1 wavefront screens 32 components); later chunks stay chunk-major.
-#ifndef RIANN_FINAL_C0
-#define RIANN_FINAL_C0 1
-#endif
 __host__ __device__ __forceinline__ int64_t pca_chunk_off(int64_t j, int c, int64_t n, int D)
 {
 #if RIANN_PCA_CHUNKMAJOR
     (void)D;
-#if RIANN_FINAL_C0 == 2
-    if (c < 2) return j * 32 + 16 * c;
-#endif
     return ((int64_t)c * n + j) * 16;
 #else
     (void)n;
@@ -1665,7 +1657,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
             {
                 float q0[16];
                 {
-                    const float4 *q4 = reinterpret_cast<const float4 *>(qp + (RIANN_FINAL_C0 == 2 ? 16 * hh : 0));
+                    const float4 *q4 = reinterpret_cast<const float4 *>(qp);
 #pragma unroll
                     for (int x = 0; x < 4; x++) {
                         const float4 t = __ldg(q4 + x);
@@ -1697,33 +1689,6 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
 #define RIANN_FINAL_FU 2
 #endif
                 constexpr int FU = RIANN_FINAL_FU;
-#if RIANN_FINAL_C0 == 2
-                // a lane pair per candidate: lane hh screens chunk hh of the 64-byte record
-                for (int e0 = 0; e0 < bn; e0 += 16 * FU) {
-                    uint4 va[FU], vb[FU];
-                    uint32_t jj[FU];
-#pragma unroll
-                    for (int u = 0; u < FU; u++) {
-                        const int e = e0 + 16 * u + (lane >> 1);
-                        jj[u] = Cj[e < bn ? e : 0];
-                        ld_keep32(SP.refs_pca16 + pca_chunk_off(jj[u], hh, P.n, D), pol_keep, va[u], vb[u]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < FU; u++) {
-                        const int e = e0 + 16 * u + (lane >> 1);
-                        float s = part16(va[u], vb[u]);
-                        s = __fadd_rn(s, __shfl_xor_sync(FULL, s, 1));
-                        const bool keep = e < bn && s <= thr;
-                        const unsigned ball = __ballot_sync(FULL, keep) & EVEN;
-                        if (keep && hh == 0) {
-                            const int o = nA + __popc(ball & lanemask_lt());
-                            Aj[o] = jj[u];
-                            As[o] = s;
-                        }
-                        nA += __popc(ball);
-                    }
-                }
-#else
                 for (int e0 = 0; e0 < bn; e0 += 32 * FU) {
                     uint4 va[FU], vb[FU];
                     uint32_t jj[FU];
@@ -1747,7 +1712,6 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
                         nA += __popc(ball);
                     }
                 }
-#endif
             }
             __syncwarp();
             // further chunks for the candidates still alive, FCW chunks per step
@@ -1756,7 +1720,7 @@ __global__ void __launch_bounds__(256, RIANN_FINAL_MINB) bulk_final_kernel(BulkP
 #define RIANN_FINAL_CW 2
 #endif
             constexpr int FCW = RIANN_FINAL_CW;
-            for (int c = RIANN_FINAL_C0; c < NCH && nA > 0; c += FCW) {
+            for (int c = 1; c < NCH && nA > 0; c += FCW) {
                 const int cn = min(FCW, NCH - c);
                 float qcs[FCW][8];
 #pragma unroll
